@@ -1,0 +1,160 @@
+/*
+ * kx.h — C ABI of the B200-native Tucker-operator / ETD3RKDS library (arXiv 2310.07551).
+ *
+ * Citations: "P:n" = line n of the paper's LaTeX source; equation labels as in
+ * the source (eq:kronsum, eq:krontomu, eq:kronsumv, ...).
+ *
+ * Problem (eq:ODE, eq:kronsum; eq:twocompdisc):
+ *     u_c'(t) = K_c u_c(t) + g_c(t, u_1, ..., u_ncomp),   K_c = A^c_d (+) ... (+) A^c_1,
+ * with A^c_mu dense n_mu x n_mu.  The library integrates it with the directionally split
+ * exponential integrators ETD2RKDS (eq:ETD2RK + eq:phisplit) and exprk3ds_real
+ * (eq:exprk3; Algorithm 1 for d = 2 with Table 1, Algorithm 2 for d > 2 with
+ * Table 3), whose hot path is the Tucker operator.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Tensors are fp64 DEVICE buffers of N = n_1*...*n_d doubles in vec order: the first index
+ *    is fastest, vec(T)[i_1 + n_1*(i_2 + n_2*(...))] = t_{i_1...i_d} ("stacks by columns",
+ *    P:187-189).  Equivalently a C-contiguous array of shape (n_d, ..., n_1).  Buffers must
+ *    be 8-byte aligned; 16-byte alignment enables the vectorised load path.
+ *  - Matrices (A_mu, L_mu) are n_mu x n_mu, column-major: L[i + j*n_mu] = l_{ij}.
+ *  - Ownership: the caller owns every tensor and matrix it passes (e.g. torch allocations
+ *    passed by data_ptr); the library never frees them and keeps no reference beyond the call,
+ *    except that kx_step caches a CUDA graph keyed on the U pointers it was given.
+ *    The library owns its context, the phi-matrix bank, its workspaces (sized by kx_set_grid /
+ *    kx_set_tau) and its internal streams/graphs.
+ *  - Streams: every compute call is enqueued asynchronously on the stream given to
+ *    kx_create (NULL = the legacy default stream) and returns immediately; use kx_sync (or
+ *    synchronise that stream) before reading results on the host.  kx_set_tau is synchronous.
+ *  - Errors: argument validation is synchronous — an invalid call returns KX_ERR_INVALID,
+ *    enqueues nothing and records a message (kx_last_error) that names mu and both extents on
+ *    shape mismatches.  Asynchronous CUDA failures surface at kx_sync or at the next call
+ *    (KX_ERR_CUDA).  A context is single-stream and not thread-safe; distinct contexts are
+ *    independent.
+ *  - Aliasing: input tensors must not alias output tensors unless stated.
+ */
+#ifndef KX_H
+#define KX_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KX_OK = 0,
+  KX_ERR_INVALID = 2,      /* bad argument / call order; nothing enqueued            */
+  KX_ERR_NUMERIC = 3,      /* non-finite state detected by kx_check_finite            */
+  KX_ERR_IO = 4,
+  KX_ERR_CUDA = 5,         /* CUDA runtime error (no device, launch failure, ...)     */
+  KX_ERR_NCCL = 6,         /* NCCL error (multi-GPU contexts)                         */
+  KX_ERR_UNSUPPORTED = 7,  /* valid request this build does not implement             */
+  KX_ERR_NOMEM = 8         /* device allocation failed                                */
+} kx_status;
+
+typedef enum {
+  KX_ETD2RKDS = 1,         /* second-order split ETD2RK, any d >= 1            */
+  KX_ETD3RKDS_REAL = 2     /* exprk3ds_real: Table 1 (d = 2) / Table 3 (d >= 3)          */
+} kx_scheme;
+
+typedef enum {
+  KX_MODEL_NONE = 0,          /* g = 0 (linear problem; ncomp any)                         */
+  KX_MODEL_SCHNAKENBERG = 1,  /* params {delta_u, delta_v, rho, a_u, a_v}     */
+  KX_MODEL_FHN = 2            /* params {delta_u, delta_v, rho, a1_v, a2_v}  */
+} kx_model;
+
+typedef struct kx_ctx kx_ctx;
+
+typedef struct {
+  long long steps;            /* kx_step calls                                           */
+  long long tucker_ops;       /* Tucker operators applied (per component)      */
+  long long mode_products;    /* mu-mode products executed (dense, per component)         */
+  long long kronsum_actions;  /* Kronecker-sum actions (per component)                    */
+  long long phi_builds;       /* small phi-matrices formed by kx_set_tau                  */
+  long long gemm_launches;    /* mode-product kernel launches                             */
+  long long other_launches;   /* elementwise / bank-assembly kernel launches              */
+  double    mode_product_flops; /* algorithmic flops of all mode products, 2*N*n_mu each */
+} kx_counters;
+
+/* ---------------------------------------------------------------- context ---------- */
+/* Create a context on CUDA device `device`, enqueueing on `cuda_stream` (a cudaStream_t,
+ * NULL = legacy default stream).  Returns KX_ERR_CUDA if the device is unavailable. */
+kx_status kx_create(kx_ctx **ctx, int device, void *cuda_stream);
+/* Free the context and everything it owns.  NULL is a no-op. */
+void kx_destroy(kx_ctx *ctx);
+/* Last error message of this context ("" if none).  Pointer valid until the next call. */
+const char *kx_last_error(const kx_ctx *ctx);
+/* Message of the last failed kx_create on this thread. */
+const char *kx_create_error(void);
+
+/* Grid: d in 1..6 directions with extents n[0..d-1] = n_1..n_d (each >= 1), ncomp in 1..4
+ * components (species).  Resets matrices, model, tau and counters. */
+kx_status kx_set_grid(kx_ctx *ctx, int d, const long long *n, int ncomp);
+/* Direction matrix A^comp_mu (mu = 1..d, comp = 0..ncomp-1), HOST column-major n_mu x n_mu,
+ * copied (host and device copies kept).  Invalidates the phi bank. */
+kx_status kx_set_direction_matrix(kx_ctx *ctx, int comp, int mu, const double *A_host);
+/* Nonlinearity g (pointwise over the components; ncomp must be 2 for the two models). */
+kx_status kx_set_model(kx_ctx *ctx, kx_model model, const double *params, int nparams);
+/* Step size tau > 0 and scheme: forms every small phi-matrix the scheme needs on the device
+ * ("Needed phi-functions" loop, P:2212-2228 / P:2285-2301) with a Taylor base approximant and
+ * the modified squaring identities of [SW09], then lays out the bank.
+ * Synchronous.  Requires all direction matrices. */
+kx_status kx_set_tau(kx_ctx *ctx, double tau, kx_scheme scheme);
+
+/* ---------------------------------------------------------------- operators -------- */
+/* mu-mode product: Y = alpha * (X x_mu L) + beta * Y, L a DEVICE column-major
+ * n_mu x n_mu matrix.  X and Y distinct; beta == 0 ignores Y's contents. */
+kx_status kx_mode_product(kx_ctx *ctx, const double *X, double *Y, int mu, const double *L,
+                          double alpha, double beta);
+/* Tucker operator: Y = alpha * (X x_1 L[0] x_2 ... x_d L[d-1]) + beta * Y.
+ * L is a HOST array of d DEVICE matrix pointers.  Modes are applied d, d-1, ..., 1
+ * (reading R2).  X and Y distinct. */
+kx_status kx_tucker(kx_ctx *ctx, const double *X, double *Y, const double *const *L,
+                    double alpha, double beta);
+/* Kronecker-sum action (eq:kronsumv): Y = K_comp X + beta * Y with the context's
+ * direction matrices of component comp.  X and Y distinct. */
+kx_status kx_kronsum(kx_ctx *ctx, int comp, const double *X, double *Y, double beta);
+/* Split phi-action from the current bank: Y = alpha * S[X] + beta * Y where
+ *   S[X] = sum_i eta_i T(X, {phi_{l_i}(c tau alpha_{i,mu} A^comp_mu)}_mu)
+ * (eq:split2d / eq:splitnd3 via eq:krontomu).  ETD3RKDS bank: ell in {1,2},
+ * stage 0: c = 1/3 (ell = 1 only), stage 1: c = 2/3, stage 2: c = 1.
+ * ETD2RKDS bank: stage must be 2 (c = 1), ell in {1,2}, second-order split (eq:secondord). */
+kx_status kx_phi_apply(kx_ctx *ctx, int comp, int ell, int stage, const double *X, double *Y,
+                       double alpha, double beta);
+/* One time step of the scheme set by kx_set_tau, in place on the ncomp DEVICE tensors U[c]
+ * (HOST array of device pointers).  t is the time at the start of the step (the built-in
+ * models are autonomous).  Replays a cached CUDA graph when the U pointers repeat. */
+kx_status kx_step(kx_ctx *ctx, double t, double *const *U);
+/* Same as kx_step but U are HOST buffers (N doubles each): copies them to the device,
+ * steps `nsteps` times, copies back, synchronises (end-to-end entry point). */
+kx_status kx_integrate_host(kx_ctx *ctx, double t0, int nsteps, double *const *U_host);
+
+/* ---------------------------------------------------------------- utilities -------- */
+kx_status kx_get_counters(const kx_ctx *ctx, kx_counters *out);
+kx_status kx_reset_counters(kx_ctx *ctx);
+/* Synchronise the context stream; returns KX_ERR_CUDA with a message on async failure. */
+kx_status kx_sync(kx_ctx *ctx);
+/* KX_ERR_NUMERIC if any entry of the device tensor X (N doubles) is NaN/Inf (synchronous). */
+kx_status kx_check_finite(kx_ctx *ctx, const double *X);
+/* Per-launch CUDA-event timing of kx_step's kernels (disables graph replay while on).
+ * kx_get_profile fills gemm_ms / other_ms (summed device time) and gemm_launches /
+ * other_launches counted since profiling was enabled, and gemm_flops (algorithmic). */
+kx_status kx_set_profiling(kx_ctx *ctx, int on);
+kx_status kx_get_profile(kx_ctx *ctx, double *gemm_ms, double *other_ms, long long *gemm_launches,
+                         long long *other_launches, double *gemm_flops);
+/* Copy one phi-matrix of the current bank to the host (column-major n_mu x n_mu, unscaled):
+ * phi_{l_term}(c tau alpha_{term,mu} A^comp_mu) for (ell, stage) as in kx_phi_apply. */
+kx_status kx_get_phi_matrix(kx_ctx *ctx, int comp, int ell, int stage, int term, int mu,
+                            double *out_host);
+
+/* Host-only (no device needed): the split coefficients the library uses.
+ * scheme KX_ETD2RKDS -> second-order single term; KX_ETD3RKDS_REAL -> Table 1 (d = 2) or
+ * Table 3 (d >= 3), "+" branch.  Writes *nterms, eta[i], inner_ell[i] and
+ * alpha[i*d + mu-1]; arrays must hold 3 terms (3*d alphas). */
+kx_status kx_scheme_coefficients(kx_scheme scheme, int ell, int d, int *nterms, double *eta,
+                                 int *inner_ell, double *alpha);
+/* Library version string. */
+const char *kx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KX_H */

@@ -1,0 +1,351 @@
+// Kernel K*1: the mu-mode product as an fp64 tensor-core GEMM on sm_100a.
+//
+// PAPER.md P:196-206 defines S = T x_mu L elementwise; "a single (full) matrix-
+// matrix product ... a single GEMM call", d of them per Tucker operator.  In vec order
+// (first index fastest) no permute is needed:
+//   mu = 1 :  Y_r = X_r * L^T      (A = X_r, k-contiguous  -> layout ROW; B = L^T row-major
+//                                    = L's column-major buffer)
+//   mu >= 2:  Y_b = L * X_b        (A = L column-major -> layout COL; B = X_b row-major
+//                                    n_mu x prod_{nu<mu} n_nu; batched over prod_{nu>mu} n_nu)
+// The split phi-actions use the same kernel with concatenated M (first mode: stacked
+// [L^1; ...; L^T] reading X once) and concatenated K (last mode: sum over terms folded into
+// the K loop, with the stage combination "+U" in the epilogue).
+//
+// fp64 tensor cores on sm_100a are reached only through the warp-level mma.sync.m8n8k4.f64
+// (SASS DMMA.8x8x4); tcgen05/UMMA has no f64 kind.  Measured on the
+// pool's B200 (profiles/peaks_r01.json): DMMA 37.1 TFLOP/s sustained, latency ~26 cycles.
+// Design: cp.async multi-stage smem pipeline (16-B chunks, zero-filled edges), padded smem rows
+// (stride = 4 mod 16 doubles -> conflict-free fragment loads for both layouts), each warp owns
+// a WM x WN accumulator block (up to 64 x 32 = 32 DMMA per k-step from 12 fragment loads),
+// epilogue C = alpha*acc + beta*D + gamma*E + diag*I with 16-B stores.
+#include "kx_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+namespace kx {
+namespace {
+
+constexpr int BK = 16;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col); fragments: a = A[g][t], b = B[t][g],
+// c = {C[g][2t], C[g][2t+1]} with g = lane/4, t = lane%4.
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
+struct Cfg {
+  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
+  static constexpr int NT = WARPS_M * WARPS_N * 32;
+  static constexpr int SA = AROW ? (BK + 4) : (BM + 4);   // smem row stride (doubles)
+  static constexpr int A_ST = AROW ? BM * SA : BK * SA;
+  static constexpr int SB = BN + 4;
+  static constexpr int B_ST = BK * SB;
+  static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8;
+  static_assert(SA % 16 == 4 && SB % 16 == 4, "conflict-free fragment loads");
+};
+
+template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
+__global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>::NT)
+    gemm_kernel(const GemmArgs p, int tiles_m, int tiles_n, int m_fastest, int z0) {
+  using C_ = Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>;
+  constexpr int NT = C_::NT, SA = C_::SA, SB = C_::SB, A_ST = C_::A_ST, B_ST = C_::B_ST;
+  constexpr int FM = WM / 8, FN = WN / 8;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + STAGES * A_ST;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm0 = (warp / C_::WARPS_N) * WM, wn0 = (warp % C_::WARPS_N) * WN;
+
+  const int tile = blockIdx.x;
+  int tm, tn;
+  if (m_fastest) {
+    tm = tile % tiles_m;
+    tn = tile / tiles_m;
+  } else {
+    tn = tile % tiles_n;
+    tm = tile / tiles_n;
+  }
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int z = z0 + blockIdx.y;
+  const int b = z % p.nb;
+  const int zt = z / p.nb;
+  const int t = zt % p.nt;
+  const int s = zt / p.nt;
+
+  const double* __restrict__ A = p.A[s] + t * p.sA_t + b * p.sA_b;
+  const double* __restrict__ B = p.B[s] + t * p.sB_t + b * p.sB_b;
+  const int M = p.M, N = p.N, kseg = p.kseg;
+  const long long lda = p.lda, ldb = p.ldb;
+  const int kps = (kseg + BK - 1) / BK;
+  const int ktiles = kps * p.nseg;
+
+  auto load_tile = [&](int kt, int stage) {
+    const int seg = kt / kps;
+    const int k0 = (kt - seg * kps) * BK;
+    double* as = As + stage * A_ST;
+    double* bs = Bs + stage * B_ST;
+    if constexpr (AROW) {
+      const double* Ab = A + p.seg_off[seg];
+      constexpr int CPR = BK / VEC;
+#pragma unroll
+      for (int it = 0; it < (BM * CPR + NT - 1) / NT; ++it) {
+        const int c = tid + it * NT;
+        if ((BM * CPR) % NT != 0 && c >= BM * CPR) break;
+        const int r = c / CPR, kc = (c % CPR) * VEC;
+        const int gm = m0 + r, gk = k0 + kc;
+        const bool v = gm < M && gk < kseg;
+        const double* src = v ? Ab + (long long)gm * lda + gk : A;
+        if constexpr (VEC == 2) cp_async16(as + r * SA + kc, src, v);
+        else cp_async8(as + r * SA + kc, src, v);
+      }
+    } else {
+      constexpr int CPR = BM / VEC;
+#pragma unroll
+      for (int it = 0; it < (BK * CPR + NT - 1) / NT; ++it) {
+        const int c = tid + it * NT;
+        if ((BK * CPR) % NT != 0 && c >= BK * CPR) break;
+        const int kr = c / CPR, mc = (c % CPR) * VEC;
+        const int gk = k0 + kr, gm = m0 + mc;
+        const bool v = gk < kseg && gm < M;
+        const double* src = v ? A + (long long)gk * lda + gm : A;
+        if constexpr (VEC == 2) cp_async16(as + kr * SA + mc, src, v);
+        else cp_async8(as + kr * SA + mc, src, v);
+      }
+    }
+    constexpr int CPRB = BN / VEC;
+    const double* Bb = B + (long long)seg * kseg * ldb;
+#pragma unroll
+    for (int it = 0; it < (BK * CPRB + NT - 1) / NT; ++it) {
+      const int c = tid + it * NT;
+      if ((BK * CPRB) % NT != 0 && c >= BK * CPRB) break;
+      const int kr = c / CPRB, nc = (c % CPRB) * VEC;
+      const int gk = k0 + kr, gn = n0 + nc;
+      const bool v = gk < kseg && gn < N;
+      const double* src = v ? Bb + (long long)gk * ldb + gn : B;
+      if constexpr (VEC == 2) cp_async16(bs + kr * SB + nc, src, v);
+      else cp_async8(bs + kr * SB + nc, src, v);
+    }
+  };
+
+  double acc[FM][FN][2];
+#pragma unroll
+  for (int i = 0; i < FM; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < ktiles) load_tile(st, st);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nk = kt + STAGES - 1;
+    if (nk < ktiles) load_tile(nk, nk % STAGES);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * A_ST;
+    const double* bs = Bs + (kt % STAGES) * B_ST;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[FM], bf[FN];
+#pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
+        else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+      }
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: C = alpha*acc + beta*D + gamma*E + diag*[m==n]
+  double* __restrict__ C = p.C[s] + t * p.sC_t + b * p.sC_b;
+  const double* D = p.D[s] ? p.D[s] + t * p.sD_t + b * p.sD_b : nullptr;
+  const double* E = p.E[s] ? p.E[s] + t * p.sE_t + b * p.sE_b : nullptr;
+  const double alpha = p.alpha, beta = p.beta, gamma = p.gamma, diag = p.diag;
+#pragma unroll
+  for (int i = 0; i < FM; ++i) {
+    const int m = m0 + wm0 + i * 8 + g;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j) {
+      const int n = n0 + wn0 + j * 8 + 2 * t4;
+      if (n >= N) continue;
+      double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+      if constexpr (VEC == 2) {
+        if (D) {
+          const double2 d2 = *reinterpret_cast<const double2*>(D + (long long)m * p.ldd + n);
+          v0 += beta * d2.x;
+          v1 += beta * d2.y;
+        }
+        if (E) {
+          const double2 e2 = *reinterpret_cast<const double2*>(E + (long long)m * p.lde + n);
+          v0 += gamma * e2.x;
+          v1 += gamma * e2.y;
+        }
+        if (m == n) v0 += diag;
+        if (m == n + 1) v1 += diag;
+        *reinterpret_cast<double2*>(C + (long long)m * p.ldc + n) = make_double2(v0, v1);
+      } else {
+        if (D) v0 += beta * D[(long long)m * p.ldd + n];
+        if (E) v0 += gamma * E[(long long)m * p.lde + n];
+        if (m == n) v0 += diag;
+        C[(long long)m * p.ldc + n] = v0;
+        if (n + 1 < N) {
+          if (D) v1 += beta * D[(long long)m * p.ldd + n + 1];
+          if (E) v1 += gamma * E[(long long)m * p.lde + n + 1];
+          if (m == n + 1) v1 += diag;
+          C[(long long)m * p.ldc + n + 1] = v1;
+        }
+      }
+    }
+  }
+}
+
+struct TileChoice {
+  int bm, bn, occ;
+  double eff;
+};
+// Resident CTAs per SM (register/smem-limited) and relative per-SM efficiency of each config.
+constexpr TileChoice kTiles[3] = {{128, 128, 1, 1.00}, {128, 64, 2, 0.97}, {64, 64, 3, 0.90}};
+
+template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
+cudaError_t prepare_cfg() {
+  using C_ = Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BM, BN, WM, WN, AROW, VEC, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  return cudaSuccess;
+}
+
+template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
+cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
+  using C_ = Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>;
+  auto kern = gemm_kernel<BM, BN, WM, WN, AROW, VEC, STAGES>;
+  cudaError_t e = prepare_cfg<BM, BN, WM, WN, AROW, VEC, STAGES>();
+  if (e != cudaSuccess) return e;
+  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
+  const long long tiles = (long long)tiles_m * tiles_n;
+  const int m_fastest = AROW ? 0 : 1;
+  for (int z0 = 0; z0 < nz; z0 += 65535) {
+    dim3 grid((unsigned)tiles, (unsigned)std::min(65535, nz - z0));
+    kern<<<grid, C_::NT, C_::SMEM, stream>>>(g, tiles_m, tiles_n, m_fastest, z0);
+  }
+  return cudaGetLastError();
+}
+
+template <bool AROW, int VEC>
+cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
+  switch (which) {
+    case 0: return launch_cfg<128, 128, 64, 32, AROW, VEC, 3>(g, nz, stream);
+    case 1: return launch_cfg<128, 64, 64, 32, AROW, VEC, 3>(g, nz, stream);
+    default: return launch_cfg<64, 64, 32, 32, AROW, VEC, 3>(g, nz, stream);
+  }
+}
+
+template <bool AROW, int VEC>
+void prepare_layout() {
+  prepare_cfg<128, 128, 64, 32, AROW, VEC, 3>();
+  prepare_cfg<128, 64, 64, 32, AROW, VEC, 3>();
+  prepare_cfg<64, 64, 32, 32, AROW, VEC, 3>();
+}
+
+int num_sms() {
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  }
+  return nsm;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+// Set the dynamic-smem attribute of every instantiation up front (kx_create), so that no
+// attribute call happens while a step is being captured into a CUDA graph.
+void gemm_prepare_all() {
+  prepare_layout<true, 2>();
+  prepare_layout<true, 1>();
+  prepare_layout<false, 2>();
+  prepare_layout<false, 1>();
+  num_sms();
+}
+
+double gemm_flops(const GemmArgs& g) {
+  return 2.0 * g.M * (double)g.N * (double)g.kseg * g.nseg * g.ns * g.nt * g.nb;
+}
+
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
+  const int nz = g.ns * g.nt * g.nb;
+  if (g.M <= 0 || g.N <= 0 || nz <= 0) return cudaSuccess;
+  if (g.kseg <= 0) return cudaErrorInvalidValue;
+  // Vector (16-B) path: every contiguous extent, leading dimension, batch stride, segment
+  // offset and base pointer must keep 2-double chunks 16-B aligned.
+  bool vec = (g.N % 2 == 0) && (g.ldb % 2 == 0) && (g.ldc % 2 == 0) && (g.ldd % 2 == 0) &&
+             (g.lde % 2 == 0) && (g.lda % 2 == 0);
+  vec = vec && (g.arow ? (g.kseg % 2 == 0) : (g.M % 2 == 0));
+  const long long strides[] = {g.sA_t, g.sA_b, g.sB_t, g.sB_b, g.sC_t, g.sC_b,
+                               g.sD_t, g.sD_b, g.sE_t, g.sE_b};
+  for (long long st : strides) vec = vec && (st % 2 == 0);
+  for (int i = 0; i < g.nseg && i < MAXSEG; ++i) vec = vec && (g.seg_off[i] % 2 == 0);
+  for (int s = 0; s < g.ns; ++s) {
+    vec = vec && aligned16(g.A[s]) && aligned16(g.B[s]) && aligned16(g.C[s]);
+    if (g.D[s]) vec = vec && aligned16(g.D[s]);
+    if (g.E[s]) vec = vec && aligned16(g.E[s]);
+  }
+  // Tile choice: minimise (waves x per-wave work) / efficiency on 148 SMs.
+  const int nsm = num_sms();
+  int best = 0;
+  double best_cost = 1e300;
+  for (int i = 0; i < 3; ++i) {
+    const TileChoice& c = kTiles[i];
+    const double tiles = (double)((g.M + c.bm - 1) / c.bm) * ((g.N + c.bn - 1) / c.bn) * nz;
+    const double waves = std::ceil(tiles / ((double)nsm * c.occ));
+    const double cost = waves * c.occ * c.bm * c.bn / c.eff;
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = i;
+    }
+  }
+  if (g.arow) return vec ? launch_layout<true, 2>(g, nz, best, stream) : launch_layout<true, 1>(g, nz, best, stream);
+  return vec ? launch_layout<false, 2>(g, nz, best, stream) : launch_layout<false, 1>(g, nz, best, stream);
+}
+
+}  // namespace kx

@@ -1,0 +1,71 @@
+// Internal declarations shared by the library's translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace kx {
+
+constexpr int MAXS = 4;        // components (species) batched in one launch
+constexpr int MAXSEG = 8;      // K segments of a concatenated-K last-mode product
+
+// One launch of the mode-product GEMM (kernel K*1):
+//   for z in [0, nz):  s = z / (nt*nb), t = (z / nb) % nt, b = z % nb
+//   C_z(m, n) = alpha * sum_k A_z(m, k) B_z(k, n) + beta * D_z(m, n) + gamma * E_z(m, n)
+//              + diag * [m == n]
+// A layout ROW ("k contiguous"): A_z(m, k) = A[seg_off[k / kseg] + m*lda + k % kseg]
+//          (K = nseg * kseg; concatenated-K over term tensors; reading 2 of §8(a) a3)
+// A layout COL ("m contiguous"): A_z(m, k) = A[k*lda + m]
+// B_z(k, n) = B[k*ldb + n];  C/D/E row-major with ldc/ldd/lde.
+// X_z = X_s[s] + t*sX_t + b*sX_b for X in {A, B, C, D, E}.
+struct GemmArgs {
+  int M = 0, N = 0, kseg = 0, nseg = 1;
+  bool arow = true;
+  const double* A[MAXS] = {};
+  const double* B[MAXS] = {};
+  double* C[MAXS] = {};
+  const double* D[MAXS] = {};
+  const double* E[MAXS] = {};
+  long long lda = 0, ldb = 0, ldc = 0, ldd = 0, lde = 0;
+  long long seg_off[MAXSEG] = {};
+  long long sA_t = 0, sA_b = 0, sB_t = 0, sB_b = 0, sC_t = 0, sC_b = 0, sD_t = 0, sD_b = 0,
+            sE_t = 0, sE_b = 0;
+  int ns = 1, nt = 1, nb = 1;
+  double alpha = 1.0, beta = 0.0, gamma = 0.0, diag = 0.0;
+};
+
+// Launch on `stream`; returns cudaSuccess or the launch error.  Chooses tile config.
+cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);
+// Algorithmic flops of a launch: 2 * M * N * K * nz.
+double gemm_flops(const GemmArgs& g);
+
+// Nonlinearity (kernel K*3): for each point i (N per component, ns <= MAXS components):
+//   mode 0:  out_c = g_c(u_1..u_ncomp)
+//   mode 1:  out_c = g_c(u) - G_c
+enum ModelId { MODEL_NONE = 0, MODEL_SCHNAKENBERG = 1, MODEL_FHN = 2 };
+struct PointwiseArgs {
+  int model = 0;
+  int ncomp = 2;
+  long long N = 0;
+  const double* u[MAXS] = {};
+  const double* G[MAXS] = {};
+  double* out[MAXS] = {};
+  double p[8] = {};
+};
+cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t stream);
+
+// Y = alpha * X (elementwise, n doubles); used for bank assembly.
+cudaError_t launch_scale(double* Y, const double* X, double alpha, long long n, cudaStream_t s);
+// Strided matrix copy with scale: Y[r*ldy + c] = alpha * X[r*ldx + c], rows x cols, batched
+// over nbatch with strides sy / sx.
+cudaError_t launch_copy2d(double* Y, long long ldy, long long sy, const double* X, long long ldx,
+                          long long sx, long long rows, long long cols, int nbatch, double alpha,
+                          cudaStream_t s);
+// Set n x n identity * v into each of nbatch matrices (stride n*n).
+cudaError_t launch_set_identity(double* Y, long long n, int nbatch, double v, cudaStream_t s);
+// flag[0] |= any(!isfinite(X[0..n)))
+cudaError_t launch_check_finite(const double* X, long long n, int* flag, cudaStream_t s);
+
+// Split coefficient tables (host).  Returns number of terms (0 if unsupported).
+int scheme_terms(int scheme, int ell, int d, double* eta, int* inner, double* alpha);
+
+}  // namespace kx

@@ -1,0 +1,175 @@
+// Kernel K*3 (nonlinearity) and small pointwise helpers.
+//
+// g is pointwise over the grid and couples the components only at a point
+// (eq:twocompdisc), so one thread handles both species at 2 consecutive points
+// with 16-B (double2) loads/stores: HBM-bound, 32 B/point for G = g(U) and 48 B/point for
+// D = g(U_s) - G.  Grid-stride over a grid sized in multiples of the SM count.
+//   Schnakenberg: g1 = rho (a_u - u + u^2 v),  g2 = rho (a_v - u^2 v)
+//   FitzHugh-Nagumo: g1 = rho (-u (u^2 - 1) - v),  g2 = rho a1 (u - a2 v)
+#include "kx_internal.h"
+
+namespace kx {
+namespace {
+
+__device__ __forceinline__ void g_point(int model, const double* p, double u, double v,
+                                        double& g1, double& g2) {
+  if (model == MODEL_SCHNAKENBERG) {
+    // p = {du, dv, rho, au, av}
+    const double u2v = u * u * v;
+    g1 = p[2] * (p[3] - u + u2v);
+    g2 = p[2] * (p[4] - u2v);
+  } else if (model == MODEL_FHN) {
+    // p = {du, dv, rho, a1, a2}
+    g1 = p[2] * (-u * (u * u - 1.0) - v);
+    g2 = p[2] * p[3] * (u - p[4] * v);
+  } else {
+    g1 = 0.0;
+    g2 = 0.0;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) nonlin2_kernel(const PointwiseArgs a) {
+  // two components, vectorised by 2 points (N even)
+  const long long n2 = a.N / 2;
+  const double2* __restrict__ u = reinterpret_cast<const double2*>(a.u[0]);
+  const double2* __restrict__ v = reinterpret_cast<const double2*>(a.u[1]);
+  double2* __restrict__ o1 = reinterpret_cast<double2*>(a.out[0]);
+  double2* __restrict__ o2 = reinterpret_cast<double2*>(a.out[1]);
+  const double2* __restrict__ G1 = reinterpret_cast<const double2*>(a.G[0]);
+  const double2* __restrict__ G2 = reinterpret_cast<const double2*>(a.G[1]);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2 uu = u[i], vv = v[i];
+    double2 r1, r2;
+    g_point(a.model, a.p, uu.x, vv.x, r1.x, r2.x);
+    g_point(a.model, a.p, uu.y, vv.y, r1.y, r2.y);
+    if (MODE == 1) {
+      const double2 h1 = G1[i], h2 = G2[i];
+      r1.x -= h1.x;
+      r1.y -= h1.y;
+      r2.x -= h2.x;
+      r2.y -= h2.y;
+    }
+    o1[i] = r1;
+    o2[i] = r2;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) nonlin_scalar_kernel(const PointwiseArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.N;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (a.ncomp == 2) {
+      double r1, r2;
+      g_point(a.model, a.p, a.u[0][i], a.u[1][i], r1, r2);
+      if (MODE == 1) {
+        r1 -= a.G[0][i];
+        r2 -= a.G[1][i];
+      }
+      a.out[0][i] = r1;
+      a.out[1][i] = r2;
+    } else {
+      for (int c = 0; c < a.ncomp; ++c) a.out[c][i] = MODE == 1 ? -a.G[c][i] : 0.0;   // g = 0 (KX_MODEL_NONE)
+    }
+  }
+}
+
+__global__ void scale_kernel(double* __restrict__ y, const double* __restrict__ x, double alpha,
+                             long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = alpha * x[i];
+}
+
+__global__ void copy2d_kernel(double* __restrict__ y, long long ldy, long long sy,
+                              const double* __restrict__ x, long long ldx, long long sx,
+                              long long rows, long long cols, double alpha) {
+  const int bz = blockIdx.y;
+  const long long total = rows * cols;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / cols, c = i % cols;
+    y[bz * sy + r * ldy + c] = alpha * x[bz * sx + r * ldx + c];
+  }
+}
+
+__global__ void set_identity_kernel(double* __restrict__ y, long long n, double v) {
+  const long long total = n * n;
+  double* yb = y + blockIdx.y * total;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    yb[i] = (i / n == i % n) ? v : 0.0;
+}
+
+__global__ void check_finite_kernel(const double* __restrict__ x, long long n, int* flag) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+int grid_for(long long work, int block) {
+  static int nsm = 0;
+  if (nsm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  }
+  long long blocks = (work + block - 1) / block;
+  const long long cap = (long long)nsm * 8;   // 8 resident 256-thread CTAs per SM
+  if (blocks > cap) blocks = cap;
+  return (int)(blocks < 1 ? 1 : blocks);
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t stream) {
+  if (a.N <= 0) return cudaSuccess;
+  bool vec = a.ncomp == 2 && a.N % 2 == 0 && al16(a.u[0]) && al16(a.u[1]) && al16(a.out[0]) &&
+             al16(a.out[1]);
+  if (mode == 1) vec = vec && al16(a.G[0]) && al16(a.G[1]);
+  if (vec) {
+    const int grid = grid_for(a.N / 2, 256);
+    if (mode == 0) nonlin2_kernel<0><<<grid, 256, 0, stream>>>(a);
+    else nonlin2_kernel<1><<<grid, 256, 0, stream>>>(a);
+  } else {
+    const int grid = grid_for(a.N, 256);
+    if (mode == 0) nonlin_scalar_kernel<0><<<grid, 256, 0, stream>>>(a);
+    else nonlin_scalar_kernel<1><<<grid, 256, 0, stream>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale(double* Y, const double* X, double alpha, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(Y, X, alpha, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy2d(double* Y, long long ldy, long long sy, const double* X, long long ldx,
+                          long long sx, long long rows, long long cols, int nbatch, double alpha,
+                          cudaStream_t s) {
+  if (rows <= 0 || cols <= 0 || nbatch <= 0) return cudaSuccess;
+  dim3 grid(grid_for(rows * cols, 256), nbatch);
+  copy2d_kernel<<<grid, 256, 0, s>>>(Y, ldy, sy, X, ldx, sx, rows, cols, alpha);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_identity(double* Y, long long n, int nbatch, double v, cudaStream_t s) {
+  if (n <= 0 || nbatch <= 0) return cudaSuccess;
+  dim3 grid(grid_for(n * n, 256), nbatch);
+  set_identity_kernel<<<grid, 256, 0, s>>>(Y, n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const double* X, long long n, int* flag, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  check_finite_kernel<<<grid_for(n, 256), 256, 0, s>>>(X, n, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace kx

@@ -1,0 +1,226 @@
+"""Thin ctypes binding of the C ABI declared in include/kx.h (argument marshalling only).
+
+Every ``kx_*`` function of the header is exposed here under the same name; ``Context`` is a
+convenience wrapper that accepts torch tensors (fp64, CUDA, contiguous; vec order = C-order
+shape (n_d, ..., n_1)) and numpy matrices (column-major is produced here with
+``np.asfortranarray``).  No arithmetic of the method happens in Python: every step runs in
+libkx.so's CUDA kernels.  If libkx.so is missing or fails to load, importing this module
+raises — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkx.so")
+
+KX_OK, KX_ERR_INVALID, KX_ERR_NUMERIC, KX_ERR_IO = 0, 2, 3, 4
+KX_ERR_CUDA, KX_ERR_NCCL, KX_ERR_UNSUPPORTED, KX_ERR_NOMEM = 5, 6, 7, 8
+KX_ETD2RKDS, KX_ETD3RKDS_REAL = 1, 2
+KX_MODEL_NONE, KX_MODEL_SCHNAKENBERG, KX_MODEL_FHN = 0, 1, 2
+
+SCHEMES = {"etd2rkds": KX_ETD2RKDS, "etd3rkds": KX_ETD3RKDS_REAL,
+           "exprk3ds_real": KX_ETD3RKDS_REAL}
+MODELS = {"none": KX_MODEL_NONE, "schnakenberg": KX_MODEL_SCHNAKENBERG, "fhn": KX_MODEL_FHN}
+
+
+class KxError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"kx status {status}: {msg}")
+        self.status = status
+
+
+class kx_counters(C.Structure):
+    _fields_ = [("steps", C.c_longlong), ("tucker_ops", C.c_longlong),
+                ("mode_products", C.c_longlong), ("kronsum_actions", C.c_longlong),
+                ("phi_builds", C.c_longlong), ("gemm_launches", C.c_longlong),
+                ("other_launches", C.c_longlong), ("mode_product_flops", C.c_double)]
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2310_07551_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+lib = C.CDLL(LIB_PATH)
+
+_vp, _dp, _i, _d, _ll = C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_double, C.c_longlong
+_SIGS = {
+    "kx_create": (_i, [C.POINTER(_vp), _i, _vp]),
+    "kx_destroy": (None, [_vp]),
+    "kx_last_error": (C.c_char_p, [_vp]),
+    "kx_create_error": (C.c_char_p, []),
+    "kx_set_grid": (_i, [_vp, _i, C.POINTER(_ll), _i]),
+    "kx_set_direction_matrix": (_i, [_vp, _i, _i, _dp]),
+    "kx_set_model": (_i, [_vp, _i, _dp, _i]),
+    "kx_set_tau": (_i, [_vp, _d, _i]),
+    "kx_mode_product": (_i, [_vp, _vp, _vp, _i, _vp, _d, _d]),
+    "kx_tucker": (_i, [_vp, _vp, _vp, C.POINTER(_vp), _d, _d]),
+    "kx_kronsum": (_i, [_vp, _i, _vp, _vp, _d]),
+    "kx_phi_apply": (_i, [_vp, _i, _i, _i, _vp, _vp, _d, _d]),
+    "kx_step": (_i, [_vp, _d, C.POINTER(_vp)]),
+    "kx_integrate_host": (_i, [_vp, _d, _i, C.POINTER(_vp)]),
+    "kx_get_counters": (_i, [_vp, C.POINTER(kx_counters)]),
+    "kx_reset_counters": (_i, [_vp]),
+    "kx_sync": (_i, [_vp]),
+    "kx_check_finite": (_i, [_vp, _vp]),
+    "kx_set_profiling": (_i, [_vp, _i]),
+    "kx_get_profile": (_i, [_vp, _dp, _dp, C.POINTER(_ll), C.POINTER(_ll), _dp]),
+    "kx_get_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
+    "kx_scheme_coefficients": (_i, [_i, _i, _i, C.POINTER(_i), _dp, C.POINTER(_i), _dp]),
+    "kx_version": (C.c_char_p, []),
+}
+EXPORTED = tuple(_SIGS)
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+    globals()[_name] = _f
+
+
+def _ptr(t) -> int:
+    """Device pointer of a torch tensor (fp64, CUDA, contiguous) or a raw int."""
+    if isinstance(t, int):
+        return t
+    if t.dtype.__repr__() != "torch.float64":
+        raise TypeError("tensors must be float64")
+    if not t.is_cuda:
+        raise TypeError("tensors must live on the GPU")
+    if not t.is_contiguous():
+        raise TypeError("tensors must be contiguous")
+    return t.data_ptr()
+
+
+def scheme_coefficients(scheme: str | int, ell: int, d: int):
+    """Host-only: (etas, inner ells, alphas[i][mu]) the library uses."""
+    sc = SCHEMES.get(scheme, scheme)
+    nt = C.c_int(0)
+    eta = (C.c_double * 3)()
+    inner = (C.c_int * 3)()
+    alpha = (C.c_double * (3 * d))()
+    st = kx_scheme_coefficients(sc, ell, d, C.byref(nt), eta, inner, alpha)
+    if st != KX_OK:
+        raise KxError(st, "scheme not available")
+    n = nt.value
+    return (list(eta[:n]), list(inner[:n]), [list(alpha[i * d:(i + 1) * d]) for i in range(n)])
+
+
+class Context:
+    """Owns one kx_ctx.  Methods mirror the C ABI one to one."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        h = C.c_void_p()
+        st = kx_create(C.byref(h), device, C.c_void_p(stream.cuda_stream))
+        if st != KX_OK:
+            raise KxError(st, kx_create_error().decode())
+        self.h = h
+        self.d = 0
+        self.n: list[int] = []
+        self.ncomp = 0
+
+    def _check(self, st: int):
+        if st != KX_OK:
+            raise KxError(st, kx_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            kx_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    # --- setup
+    def set_grid(self, n: list[int], ncomp: int = 2):
+        arr = (C.c_longlong * len(n))(*n)
+        self._check(kx_set_grid(self.h, len(n), arr, ncomp))
+        self.d, self.n, self.ncomp = len(n), list(n), ncomp
+
+    def set_direction_matrix(self, comp: int, mu: int, A: np.ndarray):
+        buf = np.ascontiguousarray(np.asarray(A, dtype=np.float64).T)   # column-major bytes
+        self._check(kx_set_direction_matrix(self.h, comp, mu,
+                                            buf.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def set_model(self, model: str, params: dict | None = None):
+        m = MODELS[model]
+        if m == KX_MODEL_NONE:
+            self._check(kx_set_model(self.h, m, None, 0))
+            return
+        keys = ("du", "dv", "rho", "au", "av") if model == "schnakenberg" else \
+               ("du", "dv", "rho", "a1", "a2")
+        vals = (C.c_double * 5)(*[params[k] for k in keys])
+        self._check(kx_set_model(self.h, m, vals, 5))
+
+    def set_tau(self, tau: float, scheme: str):
+        self._check(kx_set_tau(self.h, tau, SCHEMES[scheme]))
+
+    # --- operators (device tensors)
+    def mode_product(self, X, Y, mu: int, L, alpha=1.0, beta=0.0):
+        self._check(kx_mode_product(self.h, _ptr(X), _ptr(Y), mu, _ptr(L), alpha, beta))
+
+    def tucker(self, X, Y, Ls, alpha=1.0, beta=0.0):
+        arr = (C.c_void_p * len(Ls))(*[_ptr(L) for L in Ls])
+        self._check(kx_tucker(self.h, _ptr(X), _ptr(Y), arr, alpha, beta))
+
+    def kronsum(self, comp: int, X, Y, beta=0.0):
+        self._check(kx_kronsum(self.h, comp, _ptr(X), _ptr(Y), beta))
+
+    def phi_apply(self, comp: int, ell: int, stage: int, X, Y, alpha=1.0, beta=0.0):
+        self._check(kx_phi_apply(self.h, comp, ell, stage, _ptr(X), _ptr(Y), alpha, beta))
+
+    def step(self, U: list, t: float = 0.0):
+        arr = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
+        self._check(kx_step(self.h, t, arr))
+
+    def integrate_host(self, U_host: list[np.ndarray], nsteps: int, t0: float = 0.0):
+        """U_host: C-contiguous float64 host arrays (pinned torch tensors work too: pass
+        their .numpy()).  Updated in place."""
+        ptrs = []
+        for u in U_host:
+            if isinstance(u, np.ndarray):
+                assert u.dtype == np.float64 and u.flags.c_contiguous
+                ptrs.append(u.ctypes.data)
+            else:
+                ptrs.append(u.data_ptr())
+        arr = (C.c_void_p * len(ptrs))(*ptrs)
+        self._check(kx_integrate_host(self.h, t0, nsteps, arr))
+
+    def sync(self):
+        self._check(kx_sync(self.h))
+
+    def check_finite(self, X) -> bool:
+        st = kx_check_finite(self.h, _ptr(X))
+        if st == KX_ERR_NUMERIC:
+            return False
+        self._check(st)
+        return True
+
+    def counters(self) -> dict:
+        c = kx_counters()
+        self._check(kx_get_counters(self.h, C.byref(c)))
+        return {k: getattr(c, k) for k, _ in kx_counters._fields_}
+
+    def reset_counters(self):
+        self._check(kx_reset_counters(self.h))
+
+    def set_profiling(self, on: bool):
+        self._check(kx_set_profiling(self.h, 1 if on else 0))
+
+    def profile(self) -> dict:
+        gm, om, gf = C.c_double(), C.c_double(), C.c_double()
+        gl, ol = C.c_longlong(), C.c_longlong()
+        self._check(kx_get_profile(self.h, C.byref(gm), C.byref(om), C.byref(gl), C.byref(ol),
+                                   C.byref(gf)))
+        return dict(gemm_ms=gm.value, other_ms=om.value, gemm_launches=gl.value,
+                    other_launches=ol.value, gemm_flops=gf.value)
+
+    def phi_matrix(self, comp: int, ell: int, stage: int, term: int, mu: int) -> np.ndarray:
+        n = self.n[mu - 1]
+        out = np.empty(n * n)
+        self._check(kx_get_phi_matrix(self.h, comp, ell, stage, term, mu,
+                                      out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out.reshape(n, n, order="F")

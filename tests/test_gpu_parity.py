@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Tolerances (BASELINE.json north_star): 1e-12 relative inf-norm per Tucker
+application / mode product / Kronecker-sum action; phi-bank and split actions with two
+INDEPENDENT phi algorithms (library: Taylor theta=1 + doubling on the GPU; oracle: Taylor
+theta=2 + doubling on the CPU) agree to the phi-bank limit of DESIGN.md (1e-11 at stiff
+settings); integrations to 1e-10 relative."""
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+from oracle import coeffs
+from oracle.etd import exprk3ds_precompute, integrate, split_apply, split_phi_matrices
+from oracle.phi import phi_matrices
+from oracle.tensor import kronsum_apply, mode_product, tucker, unvec, vec
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def kx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2310_07551_b200 import build
+    build.build()
+    from paper_2310_07551_b200 import kx as mod
+    return mod
+
+
+@pytest.fixture
+def ctx(kx):
+    c = kx.Context(0)
+    yield c
+    c.close()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def dmat(A):
+    """Device column-major copy of a dense matrix."""
+    return dev(np.asarray(A).T.copy())
+
+
+def relerr(x, ref):
+    x, ref = np.asarray(x), np.asarray(ref)
+    return np.max(np.abs(x - ref)) / max(np.max(np.abs(ref)), 1e-300)
+
+
+def tensor(n, seed, stream=0):
+    return inputs.uniform_sym(seed, stream, int(np.prod(n)))
+
+
+SHAPES = [[1], [7], [64], [3, 5], [65, 33], [100, 150], [128, 128], [1, 9], [9, 1],
+          [5, 6, 7], [16, 24, 32], [33, 17, 65], [64, 64, 64], [3, 4, 5, 6], [2, 3, 2, 3, 2]]
+
+
+@pytest.mark.parametrize("n", SHAPES, ids=lambda n: "x".join(map(str, n)))
+def test_mode_product_parity(ctx, n):
+    ctx.set_grid(n, 1)
+    x = tensor(n, 1)
+    X = dev(x)
+    Xo = unvec(x, n)
+    for mu in range(1, len(n) + 1):
+        L = inputs.uniform_sym(10 + mu, 0, n[mu - 1] ** 2).reshape(n[mu - 1], n[mu - 1])
+        y0 = tensor(n, 2)
+        Y = dev(y0)
+        ctx.mode_product(X, Y, mu, dmat(L), alpha=0.75, beta=-0.5)
+        ref = 0.75 * vec(mode_product(Xo, L, mu)) - 0.5 * y0
+        assert relerr(Y.cpu().numpy(), ref) <= 1e-13, mu
+
+
+@pytest.mark.parametrize("n", SHAPES, ids=lambda n: "x".join(map(str, n)))
+def test_tucker_parity(ctx, n):
+    ctx.set_grid(n, 1)
+    x = tensor(n, 3)
+    Ls = [inputs.uniform_sym(20 + mu, 0, m * m).reshape(m, m) / math.sqrt(m)
+          for mu, m in enumerate(n)]
+    Y = dev(np.zeros(int(np.prod(n))))
+    ctx.tucker(dev(x), Y, [dmat(L) for L in Ls])
+    ref = vec(tucker(unvec(x, n), Ls))
+    assert relerr(Y.cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [[6], [64, 64], [100, 150], [33, 17, 65], [32, 32, 32], [4, 5, 3, 6]],
+                         ids=lambda n: "x".join(map(str, n)))
+def test_kronsum_parity(ctx, n):
+    ctx.set_grid(n, 2)
+    As = [[inputs.laplacian_neumann(m, 1.0, 1.0 + 9.0 * c) + 0.1 * inputs.uniform_sym(5, mu, m * m).reshape(m, m)
+           for mu, m in enumerate(n)] for c in range(2)]
+    for c in range(2):
+        for mu in range(len(n)):
+            ctx.set_direction_matrix(c, mu + 1, As[c][mu])
+    x = tensor(n, 4)
+    for c in range(2):
+        y0 = tensor(n, 6 + c)
+        Y = dev(y0)
+        ctx.kronsum(c, dev(x), Y, beta=2.0)
+        ref = vec(kronsum_apply(unvec(x, n), As[c])) + 2.0 * y0
+        assert relerr(Y.cpu().numpy(), ref) <= 1e-12
+
+
+def setup_problem(ctx, prob, scheme, tau):
+    ctx.set_grid(prob.n, 2)
+    for c in range(2):
+        for mu in range(prob.d):
+            ctx.set_direction_matrix(c, mu + 1, prob.A[c][mu])
+    ctx.set_model(prob.model, prob.params)
+    ctx.set_tau(tau, scheme)
+
+
+@pytest.mark.parametrize("case", [("schnakenberg", 2, 64, 1.0 / 3000), ("schnakenberg", 2, 150, 0.25 / 1000),
+                                  ("fhn", 3, 32, 0.015), ("fhn", 3, 65, 0.015)])
+def test_phi_bank_vs_oracle(ctx, case):
+    """Every phi-matrix of the ETD3RKDS bank against the oracle's independent phi."""
+    model, d, n, tau = case
+    prob = inputs.make_problem(model, d, n)
+    setup_problem(ctx, prob, "etd3rkds", tau)
+    s = {1: coeffs.etd3_scheme(1, d), 2: coeffs.etd3_scheme(2, d)}
+    cs = {0: 1 / 3, 1: 2 / 3, 2: 1.0}
+    worst = 0.0
+    for c in range(2):
+        for (ell, stage) in [(1, 0), (1, 1), (1, 2), (2, 1), (2, 2)]:
+            for i in range(s[ell].nterms):
+                for mu in range(1, d + 1):
+                    P = ctx.phi_matrix(c, ell, stage, i, mu)
+                    X = cs[stage] * tau * s[ell].alphas[i][mu - 1] * prob.A[c][mu - 1]
+                    ref = phi_matrices(X, 2)[s[ell].inner[i]]
+                    worst = max(worst, relerr(P, ref))
+                    rs = P.sum(axis=1) * math.factorial(s[ell].inner[i])   # row sums = 1/l!
+                    assert np.max(np.abs(rs - 1.0)) <= 1e-11
+    assert worst <= 1e-11, worst
+
+
+@pytest.mark.parametrize("case", [("schnakenberg", 2, 64, 1.0 / 3000), ("fhn", 3, 24, 0.015),
+                                  ("schnakenberg", 2, 100, 1e-3)])
+def test_phi_apply_parity(ctx, case):
+    model, d, n, tau = case
+    prob = inputs.make_problem(model, d, n)
+    setup_problem(ctx, prob, "etd3rkds", tau)
+    x = tensor(prob.n, 8)
+    cs = {0: 1 / 3, 1: 2 / 3, 2: 1.0}
+    for c in range(2):
+        for (ell, stage) in [(1, 0), (1, 1), (1, 2), (2, 1), (2, 2)]:
+            s = coeffs.etd3_scheme(ell, d)
+            P = split_phi_matrices(s, cs[stage] * tau, prob.A[c])
+            ref = vec(split_apply(s.etas, P, unvec(x, prob.n)))
+            y0 = tensor(prob.n, 9)
+            Y = dev(y0)
+            ctx.phi_apply(c, ell, stage, dev(x), Y, alpha=0.5, beta=1.0)
+            assert relerr(Y.cpu().numpy(), 0.5 * ref + y0) <= 1e-11
+
+
+def run_gpu(ctx, prob, scheme, tau, steps):
+    U = [dev(u) for u in prob.U0]
+    for k in range(steps):
+        ctx.step(U, k * tau)
+    ctx.sync()
+    return [u.cpu().numpy() for u in U]
+
+
+@pytest.mark.parametrize("case", [
+    ("schnakenberg", 2, 64, "etd2rkds", 0.25, 3000, 20),      # C1
+    ("schnakenberg", 2, 64, "etd3rkds", 2.0, 6000, 20),
+    ("schnakenberg", 2, 100, "etd3rkds", 0.25, 1000, 10),     # ragged n
+    ("fhn", 3, 32, "etd3rkds", 150.0, 10000, 20),
+    ("fhn", 3, 24, "etd2rkds", 5.0, 60000, 20),
+    ("fhn", 3, 33, "etd3rkds", 150.0, 10000, 5),              # ragged n
+])
+def test_step_parity(ctx, case):
+    model, d, n, scheme, T, m, steps = case
+    prob = inputs.make_problem(model, d, n, seed=0)
+    tau = T / m
+    setup_problem(ctx, prob, scheme, tau)
+    out = run_gpu(ctx, prob, scheme, tau, steps)
+    ref, _ = integrate(prob, scheme, T=T, m=m, steps=steps)
+    err = max(relerr(out[c], ref[c]) for c in range(2))
+    assert err <= 1e-10, err
+    cnt = ctx.counters()
+    per = 2 if scheme == "etd2rkds" else (10 if d == 2 else 15)
+    assert cnt["steps"] == steps
+    assert cnt["tucker_ops"] == steps * 2 * per
+    assert cnt["kronsum_actions"] == steps * 2
+
+
+def test_linear_cosine_closed_form_full_size(ctx):
+    """C2 size (1024^2), g = 0, cosine-mode initial data: one ETD3RKDS step is the scalar
+    recurrence of SURVEY §8(c) — a full-size check that needs no oracle run."""
+    n, delta, tau = 1024, 10.0, 1.0 / 3000
+    A = inputs.laplacian_neumann(n, 1.0, delta)
+    ks = (3, 200)
+    x = inputs.kron_vec([inputs.cosine_mode(n, k) for k in ks])
+    lams = [inputs.cosine_eigenvalue(n, 1.0, delta, k) for k in ks]
+    ctx.set_grid([n, n], 2)
+    for c in range(2):
+        for mu in (1, 2):
+            ctx.set_direction_matrix(c, mu, A)
+    ctx.set_model("none")
+    ctx.set_tau(tau, "etd3rkds")
+    U = [dev(x), dev(x)]
+    ctx.step(U)
+    ctx.sync()
+    s = coeffs.table1(1)
+
+    def phis(ell, z):
+        return [math.exp(z), math.expm1(z) / z, (math.expm1(z) - z) / (z * z)][ell]
+
+    split = sum(eta * phis(li, tau * al[0] * lams[0]) * phis(li, tau * al[1] * lams[1])
+                for eta, li, al in zip(s.etas, s.inner, s.alphas))
+    expect = (1.0 + tau * sum(lams) * split) * x
+    assert relerr(U[0].cpu().numpy(), expect) <= 1e-11
+
+
+def test_full_size_tucker_sampled(ctx):
+    """C2 size Tucker (1024^2) and C3-size (128^3): sampled outputs computed one by one."""
+    for n in ([1024, 1024], [128, 128, 128]):
+        ctx.set_grid(n, 1)
+        x = tensor(n, 11)
+        Ls = [inputs.uniform_sym(30 + mu, 0, m * m).reshape(m, m) / math.sqrt(m) for mu, m in enumerate(n)]
+        Y = dev(np.zeros(x.size))
+        ctx.tucker(dev(x), Y, [dmat(L) for L in Ls])
+        y = unvec(Y.cpu().numpy(), n)
+        X = unvec(x, n)
+        rs = np.random.default_rng(0)
+        for _ in range(64):
+            idx = [int(rs.integers(0, m)) for m in n]
+            # s_{i} = sum_j t_j prod_mu l^mu_{i_mu j_mu}
+            val = X
+            for mu in range(len(n) - 1, -1, -1):
+                val = np.tensordot(val, Ls[mu][idx[mu]], axes=([mu], [0]))
+            assert abs(y[tuple(idx)] - val) <= 1e-12 * np.max(np.abs(y))
+
+
+def test_graph_replay_matches_eager(ctx):
+    prob = inputs.make_problem("fhn", 3, 20, seed=2)
+    setup_problem(ctx, prob, "etd3rkds", 0.015)
+    Ug = [dev(u) for u in prob.U0]
+    Ue = [dev(u) for u in prob.U0]
+    for _ in range(3):
+        ctx.step(Ug)
+    ctx.set_profiling(True)
+    for _ in range(3):
+        ctx.step(Ue)
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    ctx.sync()
+    for c in range(2):
+        assert torch.equal(Ug[c], Ue[c])
+    assert prof["gemm_launches"] > 0 and prof["gemm_ms"] > 0
+
+
+def test_integrate_host_matches_device(ctx):
+    prob = inputs.make_problem("schnakenberg", 2, 48, seed=3)
+    setup_problem(ctx, prob, "etd3rkds", 1e-4)
+    Ud = [dev(u) for u in prob.U0]
+    for _ in range(4):
+        ctx.step(Ud)
+    Uh = [u.copy() for u in prob.U0]
+    ctx.integrate_host(Uh, 4)
+    for c in range(2):
+        assert np.array_equal(Uh[c], Ud[c].cpu().numpy())
+
+
+def test_equilibrium_and_finite(ctx):
+    prob = inputs.make_problem("fhn", 3, 16, amplitude=0.0)
+    setup_problem(ctx, prob, "etd3rkds", 0.015)
+    U = [dev(u) for u in prob.U0]
+    for _ in range(5):
+        ctx.step(U)
+    ctx.sync()
+    assert float(U[0].abs().max()) == 0.0 and float(U[1].abs().max()) == 0.0
+    assert ctx.check_finite(U[0])
+    bad = dev(np.array([0.0] * 16 ** 3))
+    bad[5] = float("nan")
+    assert not ctx.check_finite(bad)
+
+
+def test_invalid_arguments(ctx, kx):
+    ctx.set_grid([4, 5], 1)
+    X = dev(np.zeros(20))
+    with pytest.raises(kx.KxError, match="mode 3"):
+        ctx.mode_product(X, dev(np.zeros(20)), 3, dmat(np.eye(4)))
+    with pytest.raises(kx.KxError, match="distinct"):
+        ctx.mode_product(X, X, 1, dmat(np.eye(4)))
+    with pytest.raises(kx.KxError, match="set_tau"):
+        ctx.step([X])
+    with pytest.raises(kx.KxError):
+        ctx.set_tau(-1.0, "etd3rkds")

@@ -229,7 +229,6 @@ def test_schnakenberg_pattern():
     assert 0.55 < u.min() and u.max() < 1.85      # colour bar 0.6-1.8
 
 
-@pytest.mark.slow
 def test_fhn_pattern():
     """Fig. 7 / P:1823-1824: FHN mode (2,2,2), u within about +-0.107 at T = 150."""
     prob = inputs.make_problem("fhn", 3, 24, seed=1)
