@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark: ETD3RKDS steps/s and Tucker fp64 TFLOP/s (% of measured DMMA peak) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl kx|reference] [--config C2]
+
+Workload (BASELINE.json configs[1]): 2D Schnakenberg, 2 species,
+1024 x 1024 grid, exprk3ds_real (Algorithm 1, Table 1), tau = T/m = 2/6000, synthetic seeded
+initial data (inputs.make_problem).  One "step" = one full exprk3ds step of both species
+(1 Kronecker-sum action + 10 Tucker operators per species, 3 nonlinearity evaluations).
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the library's
+stream, with a 256 MiB L2 flush (> 126 MB L2) between steps, outside the events.  Per-kernel
+CUDA events (kx_set_profiling) over the same timed region give the dominant kernel's
+(mode-product GEMM) achieved TFLOP/s for the roofline.  e2e: the same steps through
+kx_integrate_host with pinned host buffers (H2D of U, step, D2H of U inside the timed region).
+N > 1 (torchrun): independent replicas, one per GPU (weak scaling), barrier + max over ranks.
+
+--impl reference: the CPU oracle (oracle/, numpy fp64) timed on this host's cores on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "ETD3RKDS steps/sec and Tucker fp64 TFLOP/s (% DMMA peak) at 1/2/4/8 B200"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="kx", choices=["kx", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--no-extras", action="store_true", help="skip Tucker sweep / e2e / cpu leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def config_dict(name):
+    import inputs
+    cfg = dict(inputs.CONFIGS[name])
+    return cfg
+
+
+# -------------------------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+
+        def rd():
+            for line in self.proc.stdout:
+                self.samples.append([x.strip() for x in line.split(",")])
+        self.thread = threading.Thread(target=rd, daemon=True)
+        self.thread.start()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                smax.append(float(s[1]))
+            except (ValueError, IndexError):
+                continue
+            for k, nm in enumerate(names):
+                if len(s) > 4 + k and s[4 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------------------------- oracle --
+def oracle_sample(cfg_name, seconds):
+    """Time the CPU oracle's step function on this host (bounded sample).  Returns
+    (steps_per_s, cores, sample description)."""
+    import inputs
+    from oracle.etd import Exprk3Bank, exprk3ds_step, etd2rkds_step, Etd2Bank
+    from oracle import coeffs
+    from oracle.models import g_of
+    from oracle.tensor import unvec
+    cfg = config_dict(cfg_name)
+    prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
+    tau = cfg["T"] / cfg["m"]
+    d = cfg["d"]
+    rs = np.random.default_rng(0)
+    # phi-bank formation (setup, ~7 TFLOP for C2 in the oracle) is replaced by random dense
+    # matrices of the same shapes: the per-step cost does not depend on their values.
+    if cfg["scheme"] == "etd3rkds":
+        s1, s2 = coeffs.etd3_scheme(1, d), coeffs.etd3_scheme(2, d)
+        bank = Exprk3Bank(tau, s1, s2)
+        for c in range(2):
+            Pc = {}
+            for key in [("2", 1), ("3", 1), ("3", 2), ("f", 1), ("f", 2)]:
+                Pc[key] = [[rs.uniform(0, 1.0 / n, (n, n)) for n in prob.n] for _ in range(s1.nterms)]
+            bank.P.append(Pc)
+        stepf = exprk3ds_step
+    else:
+        P = [[[rs.uniform(0, 1.0 / n, (n, n)) for n in prob.n]] for _ in range(2)]
+        bank = Etd2Bank(tau, P, P, 1.0, 2.0 ** (d - 1))
+        stepf = etd2rkds_step
+    g = g_of(prob.model)
+    U = [unvec(u, prob.n) for u in prob.U0]
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        U = stepf(U, 0.0, bank, prob.A, g, prob.params)
+        k += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    el = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    sample = (f"{k} oracle {cfg['scheme']} step(s) of {cfg_name} ({cfg['desc']}), numpy fp64 "
+              f"(BLAS matmul per mode product) on {os.cpu_count()} host cores; phi-bank formation "
+              f"excluded (random dense P of the same shapes)")
+    return k / el, cores, sample
+
+
+# -------------------------------------------------------------------------------- GPU arm --
+def load_peak():
+    p = os.path.join(ROOT, "profiles", "peaks_r01.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["dmma_tflops_sustained"]), float(j.get("hbm_copy_gbs", 0))
+    except Exception:
+        return None, None
+
+
+def load_traffic(cfg_name):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j.get(cfg_name, {}).get("gemm_dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def setup_ctx(kx, prob, scheme, tau, stream):
+    ctx = kx.Context(0 if stream is None else stream.device.index, stream)
+    ctx.set_grid(prob.n, 2)
+    for c in range(2):
+        for mu in range(prob.d):
+            ctx.set_direction_matrix(c, mu + 1, prob.A[c][mu])
+    ctx.set_model(prob.model, prob.params)
+    t0 = time.perf_counter()
+    ctx.set_tau(tau, scheme)
+    return ctx, time.perf_counter() - t0
+
+
+def tucker_sweep(kx, torch, stream, budget_s=25.0):
+    """Tucker microbenchmark at a few sizes: dense flops / event time."""
+    out = {}
+    t_start = time.perf_counter()
+    for d, n in [(2, 1024), (3, 256), (3, 512), (2, 4096)]:
+        if time.perf_counter() - t_start > budget_s:
+            break
+        import inputs
+        N = n ** d
+        ctx = kx.Context(stream.device.index, stream)
+        ctx.set_grid([n] * d, 1)
+        A = inputs.laplacian_neumann(n, np.pi, 42.1887)
+        X = torch.rand(N, dtype=torch.float64, device="cuda")
+        Y = torch.empty_like(X)
+        L = torch.rand(n * n, dtype=torch.float64, device="cuda") / n
+        Ls = [L] * d
+        reps = 3 if N * n * d > 1e11 else 10
+        for _ in range(2):
+            ctx.tucker(X, Y, Ls)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record()
+            for _ in range(reps):
+                ctx.tucker(X, Y, Ls)
+            e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        fl = 2.0 * N * n * d
+        out[f"d{d}_n{n}"] = round(fl / ms / 1e9, 2)
+        ctx.close()
+        del X, Y, L
+        torch.cuda.empty_cache()
+        del A
+    return out
+
+
+def run_kx(args, rank, world):
+    import torch
+    import inputs
+    from paper_2310_07551_b200 import kx
+
+    torch.cuda.set_device(rank % torch.cuda.device_count())
+    stream = torch.cuda.Stream()
+    cfg = config_dict(args.config)
+    prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=rank)
+    tau = cfg["T"] / cfg["m"]
+    ctx, phi_s = setup_ctx(kx, prob, cfg["scheme"], tau, stream)
+    U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")   # 256 MiB
+    torch.cuda.synchronize()
+    # warm-up (graph capture + replay)
+    for k in range(args.warmup):
+        ctx.step(U, k * tau)
+    ctx.sync()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clocks = ClockSampler(rank % max(1, torch.cuda.device_count()))
+    clocks.start()
+    time.sleep(0.3)
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            evs[k][0].record()
+            ctx.step(U, (args.warmup + k) * tau)
+            evs[k][1].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    cnt = ctx.counters()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    ok = all(ctx.check_finite(u) for u in U)
+    res = dict(ms=ms, step_ms=step_ms, prof=prof, cnt=cnt, clocks=clk, phi_s=phi_s, finite=ok)
+    # ---- e2e through kx_integrate_host with pinned host buffers
+    if not args.no_extras:
+        Uh = [torch.from_numpy(u.copy()).pin_memory() for u in prob.U0]
+        ctx.integrate_host([u.numpy() for u in Uh], 1)          # warm (graph for hostU)
+        e2e_ms = []
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.integrate_host([u.numpy() for u in Uh], 1)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        res["e2e_ms"] = sum(e2e_ms) / len(e2e_ms)
+        res["e2e_bytes"] = 2 * prob.N * 8
+    ctx.close()
+    if not args.no_extras and rank == 0:
+        del U, flush
+        torch.cuda.empty_cache()
+        res["tucker"] = tucker_sweep(kx, torch, stream)
+    return res, cfg, prob
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and world == 1:
+        print(json.dumps({"error": "run N>1 under torchrun (one process per GPU)"}))
+        return 2
+    cfg = config_dict(args.config)
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        for _ in range(args.warmup if args.warmup < 1 else 0):
+            pass
+        vals = []
+        cores = None
+        sample = ""
+        per = max(1.0, args.cpu_seconds / max(1, args.steps))
+        for k in range(max(1, args.steps)):
+            v, cores, sample = oracle_sample(args.config, per)
+            vals.append(v)
+        value = statistics.mean(vals)
+        line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "impl": "reference",
+                "config": {"workload": f"{args.config}: {cfg['desc']}", "grid": [cfg["n"]] * cfg["d"],
+                           "species": 2, "scheme": cfg["scheme"], "parallelism": "single host"},
+                "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores,
+                                 "kind": "oracle", "sample": sample},
+                "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group("nccl")
+    res, cfg, prob = run_kx(args, rank, world)
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return 0
+    value = world * 1e3 / res["ms"]
+    prof = res["prof"]
+    peak, hbm = load_peak()
+    achieved = prof["gemm_flops"] / prof["gemm_ms"] / 1e9 if prof["gemm_ms"] > 0 else None
+    launches = res["cnt"]["gemm_launches"] + res["cnt"]["other_launches"]
+    gemm_launches = prof["gemm_launches"]
+    traffic = load_traffic(args.config)
+    step_flops = res["cnt"]["mode_product_flops"] / max(1, res["cnt"]["steps"])
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 initial data, FD Neumann Laplacians; inputs/)",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "grid": prob.n, "species": 2,
+                   "scheme": cfg["scheme"], "tau": cfg["T"] / cfg["m"],
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "l2": "256 MiB buffer written between timed steps (L2 flushed)"},
+        "roofline": {"bound": "tensor", "kernel": "mode-product GEMM (fp64 DMMA mma.sync.m8n8k4)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if (achieved and peak) else None,
+                     "traffic": traffic,
+                     "peak_source": "measured fp64 DMMA, 1.5 s sustained on 148 SMs "
+                                    "(tools/peaks.cu -> profiles/peaks_r01.json); MEASURED_PEAKS.json "
+                                    "has no fp64 entry (bf16 sustained x nominal 45/2250 would give 28.0)",
+                     "gemm_share_of_step": prof["gemm_ms"] / (res["ms"] * args.steps),
+                     "gemm_launches_per_step": gemm_launches / args.steps},
+        "step_tflops": step_flops / res["ms"] / 1e9,
+        "gpu_launches": launches,
+        "clocks": res["clocks"],
+        "phi_bank_setup_s": res["phi_s"],
+        "finite": res["finite"],
+    }
+    if "e2e_ms" in res:
+        line["e2e"] = {"value": 1e3 / res["e2e_ms"], "unit": "steps/s",
+                       "h2d_bytes_per_step": res["e2e_bytes"], "d2h_bytes_per_step": res["e2e_bytes"]}
+    if "tucker" in res:
+        line["tucker_tflops"] = res["tucker"]
+        if peak:
+            line["tucker_frac_of_dmma"] = {k: round(v / peak, 3) for k, v in res["tucker"].items()}
+    if not args.no_extras:
+        v, cores, sample = oracle_sample(args.config, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
+                                "sample": sample}
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
