@@ -139,11 +139,13 @@ def oracle_sample(cfg_name, seconds):
         bank = Etd2Bank(tau, P, P, 1.0, 2.0 ** (d - 1))
         stepf = etd2rkds_step
     g = g_of(prob.model)
-    U = [unvec(u, prob.n) for u in prob.U0]
+    U0 = [unvec(u, prob.n) for u in prob.U0]
     t0 = time.perf_counter()
     k = 0
     while True:
-        U = stepf(U, 0.0, bank, prob.A, g, prob.params)
+        # every sampled step starts from the initial data (random P would otherwise let the
+        # state overflow; the cost of a step does not depend on the values)
+        stepf(U0, 0.0, bank, prob.A, g, prob.params)
         k += 1
         if time.perf_counter() - t0 >= seconds:
             break

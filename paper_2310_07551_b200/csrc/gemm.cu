@@ -27,7 +27,6 @@
 namespace kx {
 namespace {
 
-constexpr int BK = 16;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -53,7 +52,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
 struct Cfg {
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int NT = WARPS_M * WARPS_N * 32;
@@ -62,14 +61,22 @@ struct Cfg {
   static constexpr int SB = BN + 4;
   static constexpr int B_ST = BK * SB;
   static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8;
+  // loader geometry: chunks of VEC doubles, each thread owns IA (A) and IB (B) chunks
+  static constexpr int CPR_A = AROW ? BK / VEC : BM / VEC;   // chunks per smem row of A
+  static constexpr int IA = BM * BK / VEC / NT;
+  static constexpr int CPR_B = BN / VEC;
+  static constexpr int IB = BK * BN / VEC / NT;
   static_assert(SA % 16 == 4 && SB % 16 == 4, "conflict-free fragment loads");
+  static_assert((BM * BK / VEC) % NT == 0 && (BK * BN / VEC) % NT == 0, "loader divisibility");
+  static_assert(IA <= 32 && IB <= 32, "validity masks are 32-bit");
 };
 
-template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
-__global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>::NT)
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
+__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT)
     gemm_kernel(const GemmArgs p, int tiles_m, int tiles_n, int m_fastest, int z0) {
-  using C_ = Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>;
+  using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   constexpr int NT = C_::NT, SA = C_::SA, SB = C_::SB, A_ST = C_::A_ST, B_ST = C_::B_ST;
+  constexpr int IA = C_::IA, IB = C_::IB, CPR_A = C_::CPR_A, CPR_B = C_::CPR_B;
   constexpr int FM = WM / 8, FN = WN / 8;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -98,55 +105,77 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>::NT)
   const double* __restrict__ A = p.A[s] + t * p.sA_t + b * p.sA_b;
   const double* __restrict__ B = p.B[s] + t * p.sB_t + b * p.sB_b;
   const int M = p.M, N = p.N, kseg = p.kseg;
-  const long long lda = p.lda, ldb = p.ldb;
+  const int lda = (int)p.lda, ldb = (int)p.ldb;
   const int kps = (kseg + BK - 1) / BK;
   const int ktiles = kps * p.nseg;
 
-  auto load_tile = [&](int kt, int stage) {
-    const int seg = kt / kps;
-    const int k0 = (kt - seg * kps) * BK;
+  // ---- per-thread loader state: 32-bit offsets inside the operand, validity masks, and the
+  // k coordinate each chunk row adds.  Per k-tile only a pointer add + predicate remain.
+  int offA[IA], krA[IA], offB[IB], krB[IB];
+  unsigned okA = 0, okB = 0;
+#pragma unroll
+  for (int it = 0; it < IA; ++it) {
+    const int c = tid + it * NT;
+    if constexpr (AROW) {
+      const int r = c / CPR_A, kc = (c % CPR_A) * VEC;
+      const bool v = m0 + r < M;
+      offA[it] = (v ? (m0 + r) : 0) * lda + kc;
+      krA[it] = kc;
+      okA |= (unsigned)v << it;
+    } else {
+      const int kr = c / CPR_A, mc = (c % CPR_A) * VEC;
+      const bool v = m0 + mc < M;
+      offA[it] = kr * lda + (v ? m0 + mc : 0);
+      krA[it] = kr;
+      okA |= (unsigned)v << it;
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < IB; ++it) {
+    const int c = tid + it * NT;
+    const int kr = c / CPR_B, nc = (c % CPR_B) * VEC;
+    const bool v = n0 + nc < N;
+    offB[it] = kr * ldb + (v ? n0 + nc : 0);
+    krB[it] = kr;
+    okB |= (unsigned)v << it;
+  }
+  int smA[IA], smB[IB];   // smem offsets (doubles) inside a stage
+#pragma unroll
+  for (int it = 0; it < IA; ++it) {
+    const int c = tid + it * NT;
+    smA[it] = AROW ? (c / CPR_A) * SA + (c % CPR_A) * VEC : (c / CPR_A) * SA + (c % CPR_A) * VEC;
+  }
+#pragma unroll
+  for (int it = 0; it < IB; ++it) {
+    const int c = tid + it * NT;
+    smB[it] = (c / CPR_B) * SB + (c % CPR_B) * VEC;
+  }
+
+  // load cursor: (segment, k offset inside the segment)
+  int lseg = 0, lk0 = 0;
+  auto issue_loads = [&](int stage) {
     double* as = As + stage * A_ST;
     double* bs = Bs + stage * B_ST;
-    if constexpr (AROW) {
-      const double* Ab = A + p.seg_off[seg];
-      constexpr int CPR = BK / VEC;
+    const double* Ab = A + p.seg_off[lseg] + (AROW ? (long long)lk0 : (long long)lk0 * lda);
+    const double* Bb = B + ((long long)lseg * kseg + lk0) * ldb;
 #pragma unroll
-      for (int it = 0; it < (BM * CPR + NT - 1) / NT; ++it) {
-        const int c = tid + it * NT;
-        if ((BM * CPR) % NT != 0 && c >= BM * CPR) break;
-        const int r = c / CPR, kc = (c % CPR) * VEC;
-        const int gm = m0 + r, gk = k0 + kc;
-        const bool v = gm < M && gk < kseg;
-        const double* src = v ? Ab + (long long)gm * lda + gk : A;
-        if constexpr (VEC == 2) cp_async16(as + r * SA + kc, src, v);
-        else cp_async8(as + r * SA + kc, src, v);
-      }
-    } else {
-      constexpr int CPR = BM / VEC;
-#pragma unroll
-      for (int it = 0; it < (BK * CPR + NT - 1) / NT; ++it) {
-        const int c = tid + it * NT;
-        if ((BK * CPR) % NT != 0 && c >= BK * CPR) break;
-        const int kr = c / CPR, mc = (c % CPR) * VEC;
-        const int gk = k0 + kr, gm = m0 + mc;
-        const bool v = gk < kseg && gm < M;
-        const double* src = v ? A + (long long)gk * lda + gm : A;
-        if constexpr (VEC == 2) cp_async16(as + kr * SA + mc, src, v);
-        else cp_async8(as + kr * SA + mc, src, v);
-      }
+    for (int it = 0; it < IA; ++it) {
+      const bool v = ((okA >> it) & 1u) && (lk0 + krA[it] < kseg);
+      const double* src = v ? Ab + offA[it] : A;
+      if constexpr (VEC == 2) cp_async16(as + smA[it], src, v);
+      else cp_async8(as + smA[it], src, v);
     }
-    constexpr int CPRB = BN / VEC;
-    const double* Bb = B + (long long)seg * kseg * ldb;
 #pragma unroll
-    for (int it = 0; it < (BK * CPRB + NT - 1) / NT; ++it) {
-      const int c = tid + it * NT;
-      if ((BK * CPRB) % NT != 0 && c >= BK * CPRB) break;
-      const int kr = c / CPRB, nc = (c % CPRB) * VEC;
-      const int gk = k0 + kr, gn = n0 + nc;
-      const bool v = gk < kseg && gn < N;
-      const double* src = v ? Bb + (long long)gk * ldb + gn : B;
-      if constexpr (VEC == 2) cp_async16(bs + kr * SB + nc, src, v);
-      else cp_async8(bs + kr * SB + nc, src, v);
+    for (int it = 0; it < IB; ++it) {
+      const bool v = ((okB >> it) & 1u) && (lk0 + krB[it] < kseg);
+      const double* src = v ? Bb + offB[it] : B;
+      if constexpr (VEC == 2) cp_async16(bs + smB[it], src, v);
+      else cp_async8(bs + smB[it], src, v);
+    }
+    lk0 += BK;
+    if (lk0 >= kseg) {
+      lk0 = 0;
+      ++lseg;
     }
   };
 
@@ -158,18 +187,16 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>::NT)
 
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < ktiles) load_tile(st, st);
+    if (st < ktiles) issue_loads(st);
     cp_async_commit();
   }
 
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    const int nk = kt + STAGES - 1;
-    if (nk < ktiles) load_tile(nk, nk % STAGES);
-    cp_async_commit();
     const double* as = As + (kt % STAGES) * A_ST;
     const double* bs = Bs + (kt % STAGES) * B_ST;
+    const int nk = kt + STAGES - 1;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[FM], bf[FN];
@@ -184,6 +211,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>::NT)
       for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      if (kk == 0) {
+        // prefetch tile kt+STAGES-1 into the stage freed by iteration kt-1, interleaved with
+        // the DMMAs already queued for this k-step
+        if (nk < ktiles) issue_loads(nk % STAGES);
+        cp_async_commit();
+      }
     }
   }
   cp_async_wait<0>();
@@ -239,12 +272,12 @@ struct TileChoice {
 // Resident CTAs per SM (register/smem-limited) and relative per-SM efficiency of each config.
 constexpr TileChoice kTiles[3] = {{128, 128, 1, 1.00}, {128, 64, 2, 0.97}, {64, 64, 3, 0.90}};
 
-template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
 cudaError_t prepare_cfg() {
-  using C_ = Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>;
+  using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BM, BN, WM, WN, AROW, VEC, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
     if (e != cudaSuccess) return e;
     attr_done = true;
@@ -252,11 +285,11 @@ cudaError_t prepare_cfg() {
   return cudaSuccess;
 }
 
-template <int BM, int BN, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
 cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
-  using C_ = Cfg<BM, BN, WM, WN, AROW, VEC, STAGES>;
-  auto kern = gemm_kernel<BM, BN, WM, WN, AROW, VEC, STAGES>;
-  cudaError_t e = prepare_cfg<BM, BN, WM, WN, AROW, VEC, STAGES>();
+  using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>();
   if (e != cudaSuccess) return e;
   const int tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
   const long long tiles = (long long)tiles_m * tiles_n;
@@ -271,17 +304,17 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
 template <bool AROW, int VEC>
 cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
   switch (which) {
-    case 0: return launch_cfg<128, 128, 64, 32, AROW, VEC, 3>(g, nz, stream);
-    case 1: return launch_cfg<128, 64, 64, 32, AROW, VEC, 3>(g, nz, stream);
-    default: return launch_cfg<64, 64, 32, 32, AROW, VEC, 3>(g, nz, stream);
+    case 0: return launch_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>(g, nz, stream);
+    case 1: return launch_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>(g, nz, stream);
+    default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
   }
 }
 
 template <bool AROW, int VEC>
 void prepare_layout() {
-  prepare_cfg<128, 128, 64, 32, AROW, VEC, 3>();
-  prepare_cfg<128, 64, 64, 32, AROW, VEC, 3>();
-  prepare_cfg<64, 64, 32, 32, AROW, VEC, 3>();
+  prepare_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>();
+  prepare_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>();
+  prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>();
 }
 
 int num_sms() {

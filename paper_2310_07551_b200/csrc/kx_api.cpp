@@ -115,13 +115,16 @@ struct kx_ctx {
   cudaGraphExec_t gexec = nullptr;
   double* graph_U[MAXS] = {};
   long long graph_version = -1;
+  bool graph_prof = false;
   kx_counters step_delta{};
 
   // profiling
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   struct Rec { int cls; int e0, e1; double flops; };
-  std::vector<Rec> recs;
+  std::vector<Rec> recs;        // eager launches awaiting collection
+  std::vector<Rec> graph_recs;  // event pairs captured inside the step graph
+  int graph_ev_end = 0;         // pool indices [0, graph_ev_end) belong to the graph
   int ev_used = 0;
   double prof_ms[2] = {0, 0};
   long long prof_launches[2] = {0, 0};
@@ -150,6 +153,13 @@ kx_status fail(kx_ctx* c, kx_status s, const std::string& m) {
   } while (0)
 
 // ---------------------------------------------------------------- launch wrappers ---------
+// Record an event on the current launch stream; while capturing a graph the record becomes an
+// event-record node (cudaEventRecordExternal) so that it fires on every replay.
+cudaError_t record(kx_ctx* c, cudaEvent_t e) {
+  return c->cur == c->cap ? cudaEventRecordWithFlags(e, c->cur, cudaEventRecordExternal)
+                          : cudaEventRecord(e, c->cur);
+}
+
 cudaEvent_t pool_event(kx_ctx* c, int idx) {
   while ((int)c->ev_pool.size() <= idx) {
     cudaEvent_t e;
@@ -159,17 +169,20 @@ cudaEvent_t pool_event(kx_ctx* c, int idx) {
   return c->ev_pool[idx];
 }
 
+kx_status collect_profile(kx_ctx* c);
+
 kx_status run_gemm(kx_ctx* c, const GemmArgs& g) {
   const double fl = kx::gemm_flops(g);
+  if (c->profiling && c->cur == c->stream && c->ev_used > 20000) KX_TRY(collect_profile(c));
   int e0 = -1;
   if (c->profiling) {
     e0 = c->ev_used;
     c->ev_used += 2;
-    KX_CUDA(c, cudaEventRecord(pool_event(c, e0), c->cur));
+    KX_CUDA(c, record(c, pool_event(c, e0)));
   }
   KX_CUDA(c, kx::launch_gemm(g, c->cur));
   if (c->profiling) {
-    KX_CUDA(c, cudaEventRecord(pool_event(c, e0 + 1), c->cur));
+    KX_CUDA(c, record(c, pool_event(c, e0 + 1)));
     c->recs.push_back({0, e0, e0 + 1, fl});
   }
   c->cnt.gemm_launches += 1;
@@ -183,11 +196,11 @@ kx_status run_other(kx_ctx* c, F&& launch) {
   if (c->profiling) {
     e0 = c->ev_used;
     c->ev_used += 2;
-    KX_CUDA(c, cudaEventRecord(pool_event(c, e0), c->cur));
+    KX_CUDA(c, record(c, pool_event(c, e0)));
   }
   KX_CUDA(c, launch());
   if (c->profiling) {
-    KX_CUDA(c, cudaEventRecord(pool_event(c, e0 + 1), c->cur));
+    KX_CUDA(c, record(c, pool_event(c, e0 + 1)));
     c->recs.push_back({1, e0, e0 + 1, 0.0});
   }
   c->cnt.other_launches += 1;
@@ -219,6 +232,8 @@ void drop_graph(kx_ctx* c) {
   c->gexec = nullptr;
   c->graph = nullptr;
   c->graph_version = -1;
+  c->graph_recs.clear();
+  c->graph_ev_end = 0;
 }
 
 void drop_bank(kx_ctx* c) {
@@ -833,7 +848,7 @@ kx_status collect_profile(kx_ctx* c) {
     c->prof_flops += r.flops;
   }
   c->recs.clear();
-  c->ev_used = 0;
+  c->ev_used = c->gexec ? c->graph_ev_end : 0;
   return KX_OK;
 }
 
@@ -845,24 +860,26 @@ kx_status check_ptr(kx_ctx* c, const void* p, const char* what) {
 }
 
 kx_status step_impl(kx_ctx* c, double* const* U) {
-  if (c->profiling) {
-    if (c->ev_used > 20000) KX_TRY(collect_profile(c));
-    c->cur = c->stream;
-    KX_TRY(enqueue_step(c, U));
-    c->cnt.steps += 1;
-    return KX_OK;
-  }
-  bool same = c->gexec && c->graph_version == c->bank_version;
+  // The step is always replayed from a CUDA graph.  With profiling on, the graph also holds
+  // an event-record node around every kernel; after each replay the stream is synchronised
+  // and the per-kernel device times are accumulated (kx_get_profile).
+  bool same = c->gexec && c->graph_version == c->bank_version && c->graph_prof == c->profiling;
   for (int s = 0; s < c->ncomp && same; ++s) same = c->graph_U[s] == U[s];
   if (!same) {
     drop_graph(c);
+    KX_TRY(collect_profile(c));
     const kx_counters before = c->cnt;
     c->cur = c->cap;
+    c->ev_used = 0;
+    c->recs.clear();
     KX_CUDA(c, cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
     kx_status s = enqueue_step(c, U);
     cudaGraph_t gr = nullptr;
     cudaError_t e = cudaStreamEndCapture(c->cap, &gr);
     c->cur = c->stream;
+    c->graph_recs = c->recs;
+    c->graph_ev_end = c->ev_used;
+    c->recs.clear();
     if (s != KX_OK) {
       if (gr) cudaGraphDestroy(gr);
       return s;
@@ -871,6 +888,7 @@ kx_status step_impl(kx_ctx* c, double* const* U) {
     c->graph = gr;
     KX_CUDA(c, cudaGraphInstantiate(&c->gexec, c->graph, 0));
     c->graph_version = c->bank_version;
+    c->graph_prof = c->profiling;
     for (int k = 0; k < c->ncomp; ++k) c->graph_U[k] = U[k];
     // capture counted one step's launches; remember the per-step deltas and undo
     kx_counters dl = c->cnt;
@@ -893,6 +911,16 @@ kx_status step_impl(kx_ctx* c, double* const* U) {
   c->cnt.gemm_launches += c->step_delta.gemm_launches;
   c->cnt.other_launches += c->step_delta.other_launches;
   c->cnt.mode_product_flops += c->step_delta.mode_product_flops;
+  if (c->graph_prof) {
+    KX_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (const auto& r : c->graph_recs) {
+      float ms = 0;
+      KX_CUDA(c, cudaEventElapsedTime(&ms, c->ev_pool[r.e0], c->ev_pool[r.e1]));
+      c->prof_ms[r.cls] += ms;
+      c->prof_launches[r.cls] += 1;
+      c->prof_flops += r.flops;
+    }
+  }
   return KX_OK;
 }
 
