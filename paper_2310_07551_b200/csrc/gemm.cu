@@ -71,197 +71,294 @@ struct Cfg {
   static_assert(IA <= 32 && IB <= 32, "validity masks are 32-bit");
 };
 
+// Launch schedule.  persistent = 0: one output tile per CTA (grid.x = tiles, grid.y = z).
+// persistent = 1 (hybrid data-parallel + stream-K): grid.x = G co-resident CTAs; tiles
+// [0, dp_tiles) are processed whole, round-robin; the remaining tiles' k-iterations are split
+// into G_sk contiguous ranges.  A CTA whose range starts inside a tile stores its partial
+// accumulators to its workspace slot and raises its flag; the CTA that owns the tile's first
+// k-range adds the later partials in increasing-k order (deterministic), then runs the
+// epilogue.  Waits only go to higher CTA indices, whose partial comes first in their range.
+struct Sched {
+  int tiles_m = 1, tiles_n = 1, m_fastest = 0, z0 = 0;
+  int persistent = 0, G = 0, G_sk = 0, ktiles = 0;
+  long long dp_tiles = 0, sk_units = 0;
+};
+
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
-__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT)
-    gemm_kernel(const GemmArgs p, int tiles_m, int tiles_n, int m_fastest, int z0) {
+struct GemmTile {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  constexpr int NT = C_::NT, SA = C_::SA, SB = C_::SB, A_ST = C_::A_ST, B_ST = C_::B_ST;
-  constexpr int IA = C_::IA, IB = C_::IB, CPR_A = C_::CPR_A, CPR_B = C_::CPR_B;
-  constexpr int FM = WM / 8, FN = WN / 8;
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + STAGES * A_ST;
+  static constexpr int NT = C_::NT, SA = C_::SA, SB = C_::SB, A_ST = C_::A_ST, B_ST = C_::B_ST;
+  static constexpr int IA = C_::IA, IB = C_::IB, CPR_A = C_::CPR_A, CPR_B = C_::CPR_B;
+  static constexpr int FM = WM / 8, FN = WN / 8;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int wm0 = (warp / C_::WARPS_N) * WM, wn0 = (warp % C_::WARPS_N) * WN;
+  struct Coord {
+    int m0, n0, s, t, b;
+  };
 
-  const int tile = blockIdx.x;
-  int tm, tn;
-  if (m_fastest) {
-    tm = tile % tiles_m;
-    tn = tile / tiles_m;
-  } else {
-    tn = tile % tiles_n;
-    tm = tile / tiles_n;
-  }
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int z = z0 + blockIdx.y;
-  const int b = z % p.nb;
-  const int zt = z / p.nb;
-  const int t = zt % p.nt;
-  const int s = zt / p.nt;
-
-  const double* __restrict__ A = p.A[s] + t * p.sA_t + b * p.sA_b;
-  const double* __restrict__ B = p.B[s] + t * p.sB_t + b * p.sB_b;
-  const int M = p.M, N = p.N, kseg = p.kseg;
-  const int lda = (int)p.lda, ldb = (int)p.ldb;
-  const int kps = (kseg + BK - 1) / BK;
-  const int ktiles = kps * p.nseg;
-
-  // ---- per-thread loader state: 32-bit offsets inside the operand, validity masks, and the
-  // k coordinate each chunk row adds.  Per k-tile only a pointer add + predicate remain.
-  int offA[IA], krA[IA], offB[IB], krB[IB];
-  unsigned okA = 0, okB = 0;
-#pragma unroll
-  for (int it = 0; it < IA; ++it) {
-    const int c = tid + it * NT;
-    if constexpr (AROW) {
-      const int r = c / CPR_A, kc = (c % CPR_A) * VEC;
-      const bool v = m0 + r < M;
-      offA[it] = (v ? (m0 + r) : 0) * lda + kc;
-      krA[it] = kc;
-      okA |= (unsigned)v << it;
+  __device__ __forceinline__ static Coord coords(const GemmArgs& p, const Sched& sc, long long tl) {
+    const long long tmn = (long long)sc.tiles_m * sc.tiles_n;
+    const int z = sc.z0 + (int)(tl / tmn);
+    const int r = (int)(tl - (tl / tmn) * tmn);
+    int tm, tn;
+    if (sc.m_fastest) {
+      tm = r % sc.tiles_m;
+      tn = r / sc.tiles_m;
     } else {
-      const int kr = c / CPR_A, mc = (c % CPR_A) * VEC;
-      const bool v = m0 + mc < M;
-      offA[it] = kr * lda + (v ? m0 + mc : 0);
-      krA[it] = kr;
-      okA |= (unsigned)v << it;
+      tn = r % sc.tiles_n;
+      tm = r / sc.tiles_n;
     }
-  }
-#pragma unroll
-  for (int it = 0; it < IB; ++it) {
-    const int c = tid + it * NT;
-    const int kr = c / CPR_B, nc = (c % CPR_B) * VEC;
-    const bool v = n0 + nc < N;
-    offB[it] = kr * ldb + (v ? n0 + nc : 0);
-    krB[it] = kr;
-    okB |= (unsigned)v << it;
-  }
-  int smA[IA], smB[IB];   // smem offsets (doubles) inside a stage
-#pragma unroll
-  for (int it = 0; it < IA; ++it) {
-    const int c = tid + it * NT;
-    smA[it] = AROW ? (c / CPR_A) * SA + (c % CPR_A) * VEC : (c / CPR_A) * SA + (c % CPR_A) * VEC;
-  }
-#pragma unroll
-  for (int it = 0; it < IB; ++it) {
-    const int c = tid + it * NT;
-    smB[it] = (c / CPR_B) * SB + (c % CPR_B) * VEC;
+    Coord c;
+    c.m0 = tm * BM;
+    c.n0 = tn * BN;
+    c.b = z % p.nb;
+    const int zt = z / p.nb;
+    c.t = zt % p.nt;
+    c.s = zt / p.nt;
+    return c;
   }
 
-  // load cursor: (segment, k offset inside the segment)
-  int lseg = 0, lk0 = 0;
-  auto issue_loads = [&](int stage) {
-    double* as = As + stage * A_ST;
-    double* bs = Bs + stage * B_ST;
-    const double* Ab = A + p.seg_off[lseg] + (AROW ? (long long)lk0 : (long long)lk0 * lda);
-    const double* Bb = B + ((long long)lseg * kseg + lk0) * ldb;
+  // acc += sum over k-tiles [kb, ke) of the (m0, n0) tile.
+  __device__ __forceinline__ static void mainloop(const GemmArgs& p, double* smem, const Coord& cd,
+                                                  int kb, int ke, double (&acc)[FM][FN][2]) {
+    double* As = smem;
+    double* Bs = smem + STAGES * A_ST;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm0 = (warp / C_::WARPS_N) * WM, wn0 = (warp % C_::WARPS_N) * WN;
+    const int m0 = cd.m0, n0 = cd.n0;
+    const double* __restrict__ A = p.A[cd.s] + cd.t * p.sA_t + cd.b * p.sA_b;
+    const double* __restrict__ B = p.B[cd.s] + cd.t * p.sB_t + cd.b * p.sB_b;
+    const int M = p.M, N = p.N, kseg = p.kseg;
+    const int lda = (int)p.lda, ldb = (int)p.ldb;
+    const int kps = (kseg + BK - 1) / BK;
+
+    // per-thread loader state: 32-bit offsets inside the operand + validity masks; per k-tile
+    // only a pointer add and a predicate remain
+    int offA[IA], krA[IA], offB[IB], krB[IB], smA[IA], smB[IB];
+    unsigned okA = 0, okB = 0;
 #pragma unroll
     for (int it = 0; it < IA; ++it) {
-      const bool v = ((okA >> it) & 1u) && (lk0 + krA[it] < kseg);
-      const double* src = v ? Ab + offA[it] : A;
-      if constexpr (VEC == 2) cp_async16(as + smA[it], src, v);
-      else cp_async8(as + smA[it], src, v);
+      const int c = tid + it * NT;
+      if constexpr (AROW) {
+        const int r = c / CPR_A, kc = (c % CPR_A) * VEC;
+        const bool v = m0 + r < M;
+        offA[it] = (v ? (m0 + r) : 0) * lda + kc;
+        krA[it] = kc;
+        okA |= (unsigned)v << it;
+      } else {
+        const int kr = c / CPR_A, mc = (c % CPR_A) * VEC;
+        const bool v = m0 + mc < M;
+        offA[it] = kr * lda + (v ? m0 + mc : 0);
+        krA[it] = kr;
+        okA |= (unsigned)v << it;
+      }
+      smA[it] = (c / CPR_A) * SA + (c % CPR_A) * VEC;
     }
 #pragma unroll
     for (int it = 0; it < IB; ++it) {
-      const bool v = ((okB >> it) & 1u) && (lk0 + krB[it] < kseg);
-      const double* src = v ? Bb + offB[it] : B;
-      if constexpr (VEC == 2) cp_async16(bs + smB[it], src, v);
-      else cp_async8(bs + smB[it], src, v);
+      const int c = tid + it * NT;
+      const int kr = c / CPR_B, nc = (c % CPR_B) * VEC;
+      const bool v = n0 + nc < N;
+      offB[it] = kr * ldb + (v ? n0 + nc : 0);
+      krB[it] = kr;
+      okB |= (unsigned)v << it;
+      smB[it] = (c / CPR_B) * SB + (c % CPR_B) * VEC;
     }
-    lk0 += BK;
-    if (lk0 >= kseg) {
-      lk0 = 0;
-      ++lseg;
-    }
-  };
 
-  double acc[FM][FN][2];
+    int lseg = kb / kps, lk0 = (kb - (kb / kps) * kps) * BK;   // load cursor
+    auto issue_loads = [&](int stage) {
+      double* as = As + stage * A_ST;
+      double* bs = Bs + stage * B_ST;
+      const double* Ab = A + p.seg_off[lseg] + (AROW ? (long long)lk0 : (long long)lk0 * lda);
+      const double* Bb = B + ((long long)lseg * kseg + lk0) * ldb;
 #pragma unroll
-  for (int i = 0; i < FM; ++i)
-#pragma unroll
-    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-#pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < ktiles) issue_loads(st);
-    cp_async_commit();
-  }
-
-  for (int kt = 0; kt < ktiles; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    const double* as = As + (kt % STAGES) * A_ST;
-    const double* bs = Bs + (kt % STAGES) * B_ST;
-    const int nk = kt + STAGES - 1;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[FM], bf[FN];
-#pragma unroll
-      for (int i = 0; i < FM; ++i) {
-        if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
-        else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+      for (int it = 0; it < IA; ++it) {
+        const bool v = ((okA >> it) & 1u) && (lk0 + krA[it] < kseg);
+        const double* src = v ? Ab + offA[it] : A;
+        if constexpr (VEC == 2) cp_async16(as + smA[it], src, v);
+        else cp_async8(as + smA[it], src, v);
       }
 #pragma unroll
-      for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
+      for (int it = 0; it < IB; ++it) {
+        const bool v = ((okB >> it) & 1u) && (lk0 + krB[it] < kseg);
+        const double* src = v ? Bb + offB[it] : B;
+        if constexpr (VEC == 2) cp_async16(bs + smB[it], src, v);
+        else cp_async8(bs + smB[it], src, v);
+      }
+      lk0 += BK;
+      if (lk0 >= kseg) {
+        lk0 = 0;
+        ++lseg;
+      }
+    };
+
+    const int n = ke - kb;
+    __syncthreads();   // the previous tile's readers are done with every stage
 #pragma unroll
-      for (int i = 0; i < FM; ++i)
+    for (int st = 0; st < STAGES - 1; ++st) {
+      if (st < n) issue_loads(st);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < n; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      const double* as = As + (kt % STAGES) * A_ST;
+      const double* bs = Bs + (kt % STAGES) * B_ST;
+      const int nk = kt + STAGES - 1;
 #pragma unroll
-        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-      if (kk == 0) {
-        // prefetch tile kt+STAGES-1 into the stage freed by iteration kt-1, interleaved with
-        // the DMMAs already queued for this k-step
-        if (nk < ktiles) issue_loads(nk % STAGES);
-        cp_async_commit();
+      for (int kk = 0; kk < BK; kk += 4) {
+        double af[FM], bf[FN];
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
+          else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+        }
+#pragma unroll
+        for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        if (kk == 0) {
+          // prefetch tile kt+STAGES-1 into the stage freed by iteration kt-1, interleaved
+          // with the DMMAs already queued for this k-step
+          if (nk < n) issue_loads(nk % STAGES);
+          cp_async_commit();
+        }
       }
     }
+    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
 
-  // Epilogue: C = alpha*acc + beta*D + gamma*E + diag*[m==n]
-  double* __restrict__ C = p.C[s] + t * p.sC_t + b * p.sC_b;
-  const double* D = p.D[s] ? p.D[s] + t * p.sD_t + b * p.sD_b : nullptr;
-  const double* E = p.E[s] ? p.E[s] + t * p.sE_t + b * p.sE_b : nullptr;
-  const double alpha = p.alpha, beta = p.beta, gamma = p.gamma, diag = p.diag;
+  // C = alpha*acc + beta*D + gamma*E + diag*[m==n]
+  __device__ __forceinline__ static void epilogue(const GemmArgs& p, const Coord& cd,
+                                                  const double (&acc)[FM][FN][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wm0 = (warp / C_::WARPS_N) * WM, wn0 = (warp % C_::WARPS_N) * WN;
+    const int M = p.M, N = p.N;
+    double* __restrict__ C = p.C[cd.s] + cd.t * p.sC_t + cd.b * p.sC_b;
+    const double* D = p.D[cd.s] ? p.D[cd.s] + cd.t * p.sD_t + cd.b * p.sD_b : nullptr;
+    const double* E = p.E[cd.s] ? p.E[cd.s] + cd.t * p.sE_t + cd.b * p.sE_b : nullptr;
+    const double alpha = p.alpha, beta = p.beta, gamma = p.gamma, diag = p.diag;
 #pragma unroll
-  for (int i = 0; i < FM; ++i) {
-    const int m = m0 + wm0 + i * 8 + g;
-    if (m >= M) continue;
+    for (int i = 0; i < FM; ++i) {
+      const int m = cd.m0 + wm0 + i * 8 + g;
+      if (m >= M) continue;
 #pragma unroll
-    for (int j = 0; j < FN; ++j) {
-      const int n = n0 + wn0 + j * 8 + 2 * t4;
-      if (n >= N) continue;
-      double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
-      if constexpr (VEC == 2) {
-        if (D) {
-          const double2 d2 = *reinterpret_cast<const double2*>(D + (long long)m * p.ldd + n);
-          v0 += beta * d2.x;
-          v1 += beta * d2.y;
-        }
-        if (E) {
-          const double2 e2 = *reinterpret_cast<const double2*>(E + (long long)m * p.lde + n);
-          v0 += gamma * e2.x;
-          v1 += gamma * e2.y;
-        }
-        if (m == n) v0 += diag;
-        if (m == n + 1) v1 += diag;
-        *reinterpret_cast<double2*>(C + (long long)m * p.ldc + n) = make_double2(v0, v1);
-      } else {
-        if (D) v0 += beta * D[(long long)m * p.ldd + n];
-        if (E) v0 += gamma * E[(long long)m * p.lde + n];
-        if (m == n) v0 += diag;
-        C[(long long)m * p.ldc + n] = v0;
-        if (n + 1 < N) {
-          if (D) v1 += beta * D[(long long)m * p.ldd + n + 1];
-          if (E) v1 += gamma * E[(long long)m * p.lde + n + 1];
+      for (int j = 0; j < FN; ++j) {
+        const int n = cd.n0 + wn0 + j * 8 + 2 * t4;
+        if (n >= N) continue;
+        double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+        if constexpr (VEC == 2) {
+          if (D) {
+            const double2 d2 = *reinterpret_cast<const double2*>(D + (long long)m * p.ldd + n);
+            v0 += beta * d2.x;
+            v1 += beta * d2.y;
+          }
+          if (E) {
+            const double2 e2 = *reinterpret_cast<const double2*>(E + (long long)m * p.lde + n);
+            v0 += gamma * e2.x;
+            v1 += gamma * e2.y;
+          }
+          if (m == n) v0 += diag;
           if (m == n + 1) v1 += diag;
-          C[(long long)m * p.ldc + n + 1] = v1;
+          *reinterpret_cast<double2*>(C + (long long)m * p.ldc + n) = make_double2(v0, v1);
+        } else {
+          if (D) v0 += beta * D[(long long)m * p.ldd + n];
+          if (E) v0 += gamma * E[(long long)m * p.lde + n];
+          if (m == n) v0 += diag;
+          C[(long long)m * p.ldc + n] = v0;
+          if (n + 1 < N) {
+            if (D) v1 += beta * D[(long long)m * p.ldd + n + 1];
+            if (E) v1 += gamma * E[(long long)m * p.lde + n + 1];
+            if (m == n + 1) v1 += diag;
+            C[(long long)m * p.ldc + n + 1] = v1;
+          }
         }
       }
     }
+  }
+
+  __device__ __forceinline__ static void zero(double (&acc)[FM][FN][2]) {
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
+};
+
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool SKP>
+__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT)
+    gemm_kernel(const GemmArgs p, const Sched sc) {
+  using T_ = GemmTile<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  constexpr int NT = T_::NT, FM = T_::FM, FN = T_::FN;
+  extern __shared__ __align__(16) double smem[];
+  double acc[FM][FN][2];
+  const int ktiles = sc.ktiles;
+  if constexpr (!SKP) {
+    const long long tl = (long long)blockIdx.y * sc.tiles_m * sc.tiles_n + blockIdx.x;
+    const typename T_::Coord cd = T_::coords(p, sc, tl);
+    T_::zero(acc);
+    T_::mainloop(p, smem, cd, 0, ktiles, acc);
+    T_::epilogue(p, cd, acc);
+    return;
+  } else {
+  const int i = blockIdx.x, G = sc.G;
+  for (long long tl = i; tl < sc.dp_tiles; tl += G) {
+    const typename T_::Coord cd = T_::coords(p, sc, tl);
+    T_::zero(acc);
+    T_::mainloop(p, smem, cd, 0, ktiles, acc);
+    T_::epilogue(p, cd, acc);
+  }
+  const int Gs = sc.G_sk;
+  if (i >= Gs || sc.sk_units == 0) return;
+  const long long u0 = (long long)i * sc.sk_units / Gs, u1 = (long long)(i + 1) * sc.sk_units / Gs;
+  double* ws_me = p.sk_ws + (size_t)i * (FM * FN * 2 * NT);
+  for (long long u = u0; u < u1;) {
+    const long long tr = u / ktiles;
+    const int kb = (int)(u - tr * ktiles);
+    const int ke = (int)((long long)kb + (u1 - u) < ktiles ? kb + (u1 - u) : ktiles);
+    const typename T_::Coord cd = T_::coords(p, sc, sc.dp_tiles + tr);
+    T_::zero(acc);
+    T_::mainloop(p, smem, cd, kb, ke, acc);
+    if (kb > 0) {
+      // contributor: publish the partial (thread-fragment order, coalesced) and signal
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int c = 0; c < FN; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) __stcg(ws_me + ((a * FN + c) * 2 + e) * NT + threadIdx.x, acc[a][c][e]);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicExch(p.sk_flags + i, 1);
+    } else {
+      if (ke < ktiles) {
+        // owner of a split tile: add the later k-ranges' partials in increasing k
+        for (int j = i + 1; j < Gs; ++j) {
+          const long long bj = (long long)j * sc.sk_units / Gs;
+          if (bj >= (tr + 1) * ktiles) break;
+          if (threadIdx.x == 0) {
+            volatile int* f = p.sk_flags + j;
+            while (*f == 0) __nanosleep(64);
+            __threadfence();
+            *f = 0;
+          }
+          __syncthreads();
+          const double* wj = p.sk_ws + (size_t)j * (FM * FN * 2 * NT);
+#pragma unroll
+          for (int a = 0; a < FM; ++a)
+#pragma unroll
+            for (int c = 0; c < FN; ++c)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) acc[a][c][e] += __ldcg(wj + ((a * FN + c) * 2 + e) * NT + threadIdx.x);
+        }
+      }
+      T_::epilogue(p, cd, acc);
+    }
+    u += ke - kb;
+  }
   }
 }
 
@@ -277,26 +374,55 @@ cudaError_t prepare_cfg() {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
     if (e != cudaSuccess) return e;
+    if constexpr (BM == 128 && BN == 128) {
+      e = cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
+      if (e != cudaSuccess) return e;
+    }
     attr_done = true;
   }
   return cudaSuccess;
 }
 
+int num_sms();
+
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
-cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
+cudaError_t launch_cfg(const GemmArgs& g, int nz, bool allow_sk, cudaStream_t stream) {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, false>;
   cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>();
   if (e != cudaSuccess) return e;
-  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN;
-  const long long tiles = (long long)tiles_m * tiles_n;
-  const int m_fastest = AROW ? 0 : 1;
+  Sched sc;
+  sc.tiles_m = (g.M + BM - 1) / BM;
+  sc.tiles_n = (g.N + BN - 1) / BN;
+  sc.m_fastest = AROW ? 0 : 1;
+  sc.ktiles = ((g.kseg + BK - 1) / BK) * g.nseg;
+  const long long tmn = (long long)sc.tiles_m * sc.tiles_n;
+  const long long T = tmn * nz;
+  const int G = num_sms();   // 1 CTA/SM for the configs that allow stream-K
+  if (allow_sk && g.sk_ws && g.sk_flags && G <= kSkSlots && T % G != 0 && sc.ktiles >= 8) {
+    const double waves = (double)T / G;
+    const double quant = std::ceil(waves) / waves;   // classic-schedule slowdown
+    if (quant > 1.06) {
+      long long dp = (T / G) * G;
+      if (dp >= G && (T - dp) * 2 < G) dp -= G;      // short tail: spread one more wave
+      sc.persistent = 1;
+      sc.G = G;
+      sc.dp_tiles = dp;
+      sc.sk_units = (T - dp) * sc.ktiles;
+      sc.G_sk = (int)std::min<long long>(G, sc.sk_units / 4);
+      if constexpr (BM == 128 && BN == 128)
+        gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, true><<<dim3(G, 1), C_::NT, C_::SMEM, stream>>>(g, sc);
+      return cudaGetLastError();
+    }
+  }
   for (int z0 = 0; z0 < nz; z0 += 65535) {
-    dim3 grid((unsigned)tiles, (unsigned)std::min(65535, nz - z0));
-    kern<<<grid, C_::NT, C_::SMEM, stream>>>(g, tiles_m, tiles_n, m_fastest, z0);
+    sc.z0 = z0;
+    dim3 grid((unsigned)tmn, (unsigned)std::min(65535, nz - z0));
+    kern<<<grid, C_::NT, C_::SMEM, stream>>>(g, sc);
   }
   return cudaGetLastError();
 }
@@ -304,9 +430,9 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
 template <bool AROW, int VEC>
 cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
   switch (which) {
-    case 0: return launch_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>(g, nz, stream);
-    case 1: return launch_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>(g, nz, stream);
-    default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
+    case 0: return launch_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>(g, nz, true, stream);
+    case 1: return launch_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>(g, nz, false, stream);
+    default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, false, stream);
   }
 }
 
@@ -318,7 +444,7 @@ void prepare_layout() {
 }
 
 int num_sms() {
-  static int nsm = 0;
+  static int nsm = 0;   // defined once; declared above for launch_cfg
   if (nsm == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -370,7 +496,10 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   for (int i = 0; i < 3; ++i) {
     const TileChoice& c = kTiles[i];
     const double tiles = (double)((g.M + c.bm - 1) / c.bm) * ((g.N + c.bn - 1) / c.bn) * nz;
-    const double waves = std::ceil(tiles / ((double)nsm * c.occ));
+    double waves = std::ceil(tiles / ((double)nsm * c.occ));
+    const int kt = (g.kseg + 31) / 32 * g.nseg;
+    if (i == 0 && g.sk_ws && kt >= 8 && waves / (tiles / nsm) > 1.06)
+      waves = 1.03 * tiles / nsm;   // stream-K tail: ~3% fix-up overhead
     const double cost = waves * c.occ * c.bm * c.bn / c.eff;
     if (cost < best_cost * 0.999) {
       best_cost = cost;

@@ -107,6 +107,8 @@ struct kx_ctx {
   std::vector<double*> ws_allocs;
   double* hostU[MAXS] = {};
   int* flag = nullptr;
+  double* sk_ws = nullptr;      // stream-K partial tiles (kx::kSkSlots x 128 x 128)
+  int* sk_flags = nullptr;      // stream-K flags (zero between launches)
 
   kx_counters cnt{};
 
@@ -171,7 +173,10 @@ cudaEvent_t pool_event(kx_ctx* c, int idx) {
 
 kx_status collect_profile(kx_ctx* c);
 
-kx_status run_gemm(kx_ctx* c, const GemmArgs& g) {
+kx_status run_gemm(kx_ctx* c, const GemmArgs& g_in) {
+  GemmArgs g = g_in;
+  g.sk_ws = c->sk_ws;
+  g.sk_flags = c->sk_flags;
   const double fl = kx::gemm_flops(g);
   if (c->profiling && c->cur == c->stream && c->ev_used > 20000) KX_TRY(collect_profile(c));
   int e0 = -1;
@@ -962,6 +967,10 @@ kx_status kx_create(kx_ctx** out, int device, void* cuda_stream) {
   c->cur = c->stream;
   e = cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->flag), sizeof(int));
+  if (e == cudaSuccess)
+    e = cudaMalloc(reinterpret_cast<void**>(&c->sk_ws), sizeof(double) * kx::kSkSlots * 128 * 128);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->sk_flags), sizeof(int) * kx::kSkSlots);
+  if (e == cudaSuccess) e = cudaMemset(c->sk_flags, 0, sizeof(int) * kx::kSkSlots);
   if (e != cudaSuccess) {
     g_create_error = std::string("context setup: ") + cudaGetErrorString(e);
     delete c;
@@ -984,6 +993,8 @@ void kx_destroy(kx_ctx* c) {
   for (int s = 0; s < MAXS; ++s)
     if (c->hostU[s]) cudaFree(c->hostU[s]);
   if (c->flag) cudaFree(c->flag);
+  if (c->sk_ws) cudaFree(c->sk_ws);
+  if (c->sk_flags) cudaFree(c->sk_flags);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->cap) cudaStreamDestroy(c->cap);
   delete c;

@@ -31,7 +31,11 @@ struct GemmArgs {
             sE_t = 0, sE_b = 0;
   int ns = 1, nt = 1, nb = 1;
   double alpha = 1.0, beta = 0.0, gamma = 0.0, diag = 0.0;
+  // stream-K scratch (library-owned, per context): kSkSlots x 128 x 128 doubles + flags
+  double* sk_ws = nullptr;
+  int* sk_flags = nullptr;
 };
+constexpr int kSkSlots = 160;   // >= SM count (148)
 
 // Launch on `stream`; returns cudaSuccess or the launch error.  Chooses tile config.
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);

@@ -290,3 +290,25 @@ def test_invalid_arguments(ctx, kx):
         ctx.step([X])
     with pytest.raises(kx.KxError):
         ctx.set_tau(-1.0, "etd3rkds")
+
+
+@pytest.mark.parametrize("n", [[1000, 1000], [700, 1500], [1024, 1024], [256, 200, 300], [520, 96, 40]],
+                         ids=lambda n: "x".join(map(str, n)))
+def test_streamk_shapes_parity_and_determinism(ctx, n):
+    """Shapes whose tile count is not a multiple of the SM count take the hybrid
+    data-parallel + stream-K schedule (partials reduced in fixed k order): parity with the
+    oracle and bitwise run-to-run determinism."""
+    ctx.set_grid(n, 1)
+    x = tensor(n, 12)
+    X = dev(x)
+    Xo = unvec(x, n)
+    for mu in range(1, len(n) + 1):
+        L = inputs.uniform_sym(40 + mu, 0, n[mu - 1] ** 2).reshape(n[mu - 1], n[mu - 1])
+        Ld = dmat(L)
+        Y1 = dev(np.zeros(x.size))
+        Y2 = dev(np.zeros(x.size))
+        ctx.mode_product(X, Y1, mu, Ld)
+        ctx.mode_product(X, Y2, mu, Ld)
+        ref = vec(mode_product(Xo, L, mu))
+        assert relerr(Y1.cpu().numpy(), ref) <= 1e-13, mu
+        assert torch.equal(Y1, Y2)
