@@ -112,6 +112,11 @@ kx_status kx_tucker(kx_ctx *ctx, const double *X, double *Y, const double *const
 /* Kronecker-sum action (eq:kronsumv): Y = K_comp X + beta * Y with the context's
  * direction matrices of component comp.  X and Y distinct. */
 kx_status kx_kronsum(kx_ctx *ctx, int comp, const double *X, double *Y, double beta);
+/* How the Kronecker-sum action (kx_kronsum and the F = K U + G of kx_step) is executed:
+ * mode 0 (default) uses a fused stencil kernel when every A^c_mu is tridiagonal (as for the FD
+ * Laplacians of Sec. 3) — the dense mode products would only add exact zeros —
+ * and d dense mode products otherwise; mode 1 always uses the dense mode products. */
+kx_status kx_set_kronsum_mode(kx_ctx *ctx, int mode);
 /* Split phi-action from the current bank: Y = alpha * S[X] + beta * Y where
  *   S[X] = sum_i eta_i T(X, {phi_{l_i}(c tau alpha_{i,mu} A^comp_mu)}_mu)
  * (eq:split2d / eq:splitnd3 via eq:krontomu).  ETD3RKDS bank: ell in {1,2},

@@ -78,6 +78,8 @@ struct kx_ctx {
   long long N = 0;
   std::vector<std::vector<std::vector<double>>> A_host;   // [c][mu]
   std::vector<std::vector<double*>> A_dev;                 // [c][mu]
+  std::vector<std::vector<double*>> A_tri;                 // [c][mu]: lo|di|up (3 n) or null
+  int kronsum_mode = 0;   // 0 auto (tridiagonal stencil when every A is tridiagonal), 1 dense
 
   int model = 0;
   double params[8] = {};
@@ -321,8 +323,41 @@ kx_status mode_product_multi(kx_ctx* c, int ns, const double* const* X, double* 
 
 // ---------------------------------------------------------------- Kronecker sum ------------
 // Y_s = K_{comp0+s} X_s + beta * Dd_s  for s < ns   (eq:kronsumv: sum_mu X x_mu A_mu)
+bool all_tridiag(const kx_ctx* c, int comp0, int ns) {
+  if (c->kronsum_mode != 0) return false;
+  for (int s = 0; s < ns; ++s)
+    for (int mu = 0; mu < c->d; ++mu)
+      if (!c->A_tri[comp0 + s][mu]) return false;
+  return true;
+}
+
 kx_status kronsum_multi(kx_ctx* c, int comp0, int ns, const double* const* X, double* const* Y,
                         double beta, const double* const* Dd) {
+  if (all_tridiag(c, comp0, ns)) {
+    // every A_mu is tridiagonal: the dense mode products would only add exact zeros
+    kx::StencilArgs a;
+    a.d = c->d;
+    a.ns = ns;
+    a.N = c->N;
+    a.beta = beta;
+    for (int mu = 0; mu < c->d; ++mu) a.n[mu] = c->n[mu];
+    for (int s = 0; s < ns; ++s) {
+      a.X[s] = X[s];
+      a.Y[s] = Y[s];
+      a.Dd[s] = (Dd && beta != 0.0) ? Dd[s] : nullptr;
+      for (int mu = 0; mu < c->d; ++mu) {
+        const double* t = c->A_tri[comp0 + s][mu];
+        const long long n = c->n[mu];
+        a.lo[s][mu] = t;
+        a.di[s][mu] = t + n;
+        a.up[s][mu] = t + 2 * n;
+      }
+    }
+    KX_TRY(run_other(c, [&] { return kx::launch_kronsum_tridiag(a, c->cur); }));
+    c->cnt.mode_products += (long long)ns * c->d;
+    c->cnt.kronsum_actions += ns;
+    return KX_OK;
+  }
   const double* L[MAXS];
   for (int mu = c->d; mu >= 1; --mu) {
     for (int s = 0; s < ns; ++s) L[s] = c->A_dev[comp0 + s][mu - 1];
@@ -988,6 +1023,8 @@ void kx_destroy(kx_ctx* c) {
   drop_bank(c);
   for (auto& v : c->A_dev)
     for (double* p : v) cudaFree(p);
+  for (auto& v : c->A_tri)
+    for (double* p : v) cudaFree(p);
   if (c->tmp1) cudaFree(c->tmp1);
   if (c->tmp2) cudaFree(c->tmp2);
   for (int s = 0; s < MAXS; ++s)
@@ -1019,7 +1056,10 @@ kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
   drop_bank(c);
   for (auto& v : c->A_dev)
     for (double* p : v) cudaFree(p);
+  for (auto& v : c->A_tri)
+    for (double* p : v) cudaFree(p);
   c->A_dev.clear();
+  c->A_tri.clear();
   c->A_host.clear();
   if (c->tmp1) cudaFree(c->tmp1);
   if (c->tmp2) cudaFree(c->tmp2);
@@ -1034,6 +1074,7 @@ kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
   c->N = N;
   c->A_host.assign(ncomp, std::vector<std::vector<double>>(d));
   c->A_dev.assign(ncomp, std::vector<double*>(d, nullptr));
+  c->A_tri.assign(ncomp, std::vector<double*>(d, nullptr));
   c->model = 0;
   c->cnt = kx_counters{};
   std::vector<double*> keep;
@@ -1059,6 +1100,29 @@ kx_status kx_set_direction_matrix(kx_ctx* c, int comp, int mu, const double* A_h
     KX_TRY(dalloc(c, &c->A_dev[comp][mu - 1], (size_t)(n * n), keep));
   }
   KX_CUDA(c, cudaMemcpy(c->A_dev[comp][mu - 1], A_host, n * n * 8, cudaMemcpyHostToDevice));
+  // tridiagonal? keep lo | di | up for the stencil form of the Kronecker-sum action
+  bool tri = true;
+  for (long long j = 0; j < n && tri; ++j)
+    for (long long i = 0; i < n; ++i)
+      if ((i - j > 1 || j - i > 1) && A_host[i + j * n] != 0.0) {
+        tri = false;
+        break;
+      }
+  if (c->A_tri[comp][mu - 1]) {
+    cudaFree(c->A_tri[comp][mu - 1]);
+    c->A_tri[comp][mu - 1] = nullptr;
+  }
+  if (tri) {
+    std::vector<double> t(3 * n, 0.0);
+    for (long long i = 0; i < n; ++i) {
+      if (i > 0) t[i] = A_host[i + (i - 1) * n];
+      t[n + i] = A_host[i + i * n];
+      if (i + 1 < n) t[2 * n + i] = A_host[i + (i + 1) * n];
+    }
+    std::vector<double*> keep;
+    KX_TRY(dalloc(c, &c->A_tri[comp][mu - 1], (size_t)(3 * n), keep));
+    KX_CUDA(c, cudaMemcpy(c->A_tri[comp][mu - 1], t.data(), 3 * n * 8, cudaMemcpyHostToDevice));
+  }
   return KX_OK;
 }
 
@@ -1162,6 +1226,14 @@ kx_status kx_kronsum(kx_ctx* c, int comp, const double* X, double* Y, double bet
   double* Ys[1] = {Y};
   const double* Ds[1] = {Y};
   return kronsum_multi(c, comp, 1, Xs, Ys, beta, Ds);
+}
+
+kx_status kx_set_kronsum_mode(kx_ctx* c, int mode) {
+  if (!c) return KX_ERR_INVALID;
+  if (mode != 0 && mode != 1) return fail(c, KX_ERR_INVALID, "kronsum mode must be 0 or 1");
+  if (c->kronsum_mode != mode) drop_graph(c);
+  c->kronsum_mode = mode;
+  return KX_OK;
 }
 
 kx_status kx_phi_apply(kx_ctx* c, int comp, int ell, int stage, const double* X, double* Y,

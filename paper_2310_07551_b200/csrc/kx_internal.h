@@ -57,6 +57,25 @@ struct PointwiseArgs {
 };
 cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t stream);
 
+// Kronecker-sum action with TRIDIAGONAL A_mu: for each component s,
+//   Y_s = beta * Dd_s + sum_{mu=d..1} (lo_mu[i] X[.., i-1, ..] + di_mu[i] X[.., i, ..]
+//                                     + up_mu[i] X[.., i+1, ..])
+// the same sum as eq:kronsumv with the exact zeros of a tridiagonal A_mu skipped.
+// lo/di/up: device arrays of n_mu doubles (lo[0] and up[n-1] unused).
+struct StencilArgs {
+  int d = 0, ns = 1;
+  long long n[6] = {1, 1, 1, 1, 1, 1};
+  long long N = 0;
+  const double* X[MAXS] = {};
+  double* Y[MAXS] = {};
+  const double* Dd[MAXS] = {};
+  const double* lo[MAXS][6] = {};
+  const double* di[MAXS][6] = {};
+  const double* up[MAXS][6] = {};
+  double beta = 0.0;
+};
+cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream);
+
 // Y = alpha * X (elementwise, n doubles); used for bank assembly.
 cudaError_t launch_scale(double* Y, const double* X, double alpha, long long n, cudaStream_t s);
 // Strided matrix copy with scale: Y[r*ldy + c] = alpha * X[r*ldx + c], rows x cols, batched

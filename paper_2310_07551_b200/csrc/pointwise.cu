@@ -110,6 +110,58 @@ __global__ void check_finite_kernel(const double* __restrict__ x, long long n, i
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
+// Tridiagonal Kronecker-sum action.  One CTA row-loop over "lines" (fixed i_2..i_d),
+// threads along the contiguous i_1: every load is coalesced along i_1 and the i_mu +- 1
+// neighbours (mu >= 2) are other lines read by neighbouring CTAs, so each X element is fetched
+// from HBM about once.  HBM-bound: 8 B (X) + 8 B (Dd) + 8 B (Y) per point.
+__global__ void __launch_bounds__(256) kronsum_tridiag_kernel(const StencilArgs a) {
+  const int s = blockIdx.y;
+  const double* __restrict__ X = a.X[s];
+  double* __restrict__ Y = a.Y[s];
+  const double* __restrict__ Dd = a.Dd[s];
+  const long long n1 = a.n[0];
+  const long long lines = a.N / n1;
+  for (long long line = blockIdx.x; line < lines; line += gridDim.x) {
+    // multi-index of the line and the strides of each direction
+    long long rem = line, stride = n1;
+    long long idx[6], str[6];
+    idx[0] = 0;
+    str[0] = 1;
+#pragma unroll
+    for (int mu = 1; mu < 6; ++mu) {
+      if (mu < a.d) {
+        idx[mu] = rem % a.n[mu];
+        rem /= a.n[mu];
+        str[mu] = stride;
+        stride *= a.n[mu];
+      }
+    }
+    const long long base = line * n1;
+    for (long long i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
+      const long long p = base + i1;
+      double acc = Dd ? a.beta * Dd[p] : 0.0;
+      // mu = d .. 2 (descending, as the dense path)
+#pragma unroll
+      for (int mu = 5; mu >= 1; --mu) {
+        if (mu < a.d) {
+          const long long i = idx[mu], nm = a.n[mu], st = str[mu];
+          double t = a.di[s][mu][i] * X[p];
+          if (i > 0) t = fma(a.lo[s][mu][i], X[p - st], t);
+          if (i + 1 < nm) t = fma(a.up[s][mu][i], X[p + st], t);
+          acc += t;
+        }
+      }
+      {
+        double t = a.di[s][0][i1] * X[p];
+        if (i1 > 0) t = fma(a.lo[s][0][i1], X[p - 1], t);
+        if (i1 + 1 < n1) t = fma(a.up[s][0][i1], X[p + 1], t);
+        acc += t;
+      }
+      Y[p] = acc;
+    }
+  }
+}
+
 int grid_for(long long work, int block) {
   static int nsm = 0;
   if (nsm == 0) {
@@ -141,6 +193,17 @@ cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t s
     if (mode == 0) nonlin_scalar_kernel<0><<<grid, 256, 0, stream>>>(a);
     else nonlin_scalar_kernel<1><<<grid, 256, 0, stream>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream) {
+  if (a.N <= 0) return cudaSuccess;
+  const long long lines = a.N / a.n[0];
+  const int block = a.n[0] >= 256 ? 256 : (a.n[0] >= 128 ? 128 : 64);
+  long long g = lines;
+  const long long cap = 148LL * 16;
+  if (g > cap) g = cap;
+  kronsum_tridiag_kernel<<<dim3((unsigned)g, a.ns), block, 0, stream>>>(a);
   return cudaGetLastError();
 }
 

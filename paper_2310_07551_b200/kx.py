@@ -58,6 +58,7 @@ _SIGS = {
     "kx_mode_product": (_i, [_vp, _vp, _vp, _i, _vp, _d, _d]),
     "kx_tucker": (_i, [_vp, _vp, _vp, C.POINTER(_vp), _d, _d]),
     "kx_kronsum": (_i, [_vp, _i, _vp, _vp, _d]),
+    "kx_set_kronsum_mode": (_i, [_vp, _i]),
     "kx_phi_apply": (_i, [_vp, _i, _i, _i, _vp, _vp, _d, _d]),
     "kx_step": (_i, [_vp, _d, C.POINTER(_vp)]),
     "kx_integrate_host": (_i, [_vp, _d, _i, C.POINTER(_vp)]),
@@ -168,6 +169,9 @@ class Context:
 
     def kronsum(self, comp: int, X, Y, beta=0.0):
         self._check(kx_kronsum(self.h, comp, _ptr(X), _ptr(Y), beta))
+
+    def set_kronsum_mode(self, dense: bool):
+        self._check(kx_set_kronsum_mode(self.h, 1 if dense else 0))
 
     def phi_apply(self, comp: int, ell: int, stage: int, X, Y, alpha=1.0, beta=0.0):
         self._check(kx_phi_apply(self.h, comp, ell, stage, _ptr(X), _ptr(Y), alpha, beta))

@@ -104,6 +104,28 @@ def test_kronsum_parity(ctx, n):
         assert relerr(Y.cpu().numpy(), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("n", [[7], [64, 64], [100, 150], [33, 17, 65], [32, 32, 32], [4, 5, 3, 6]],
+                         ids=lambda n: "x".join(map(str, n)))
+@pytest.mark.parametrize("dense", [False, True])
+def test_kronsum_tridiagonal_parity(ctx, n, dense):
+    """FD Neumann Laplacians (tridiagonal): the stencil path and the dense-GEMM path."""
+    ctx.set_grid(n, 2)
+    ctx.set_kronsum_mode(dense)
+    As = [[inputs.laplacian_neumann(m, 1.0, 1.0 + 9.0 * c + mu) for mu, m in enumerate(n)]
+          for c in range(2)]
+    for c in range(2):
+        for mu in range(len(n)):
+            ctx.set_direction_matrix(c, mu + 1, As[c][mu])
+    x = tensor(n, 14)
+    for c in range(2):
+        for beta in (0.0, -1.5):
+            y0 = tensor(n, 15 + c)
+            Y = dev(y0)
+            ctx.kronsum(c, dev(x), Y, beta=beta)
+            ref = vec(kronsum_apply(unvec(x, n), As[c])) + beta * y0
+            assert relerr(Y.cpu().numpy(), ref) <= 1e-12
+
+
 def setup_problem(ctx, prob, scheme, tau):
     ctx.set_grid(prob.n, 2)
     for c in range(2):
