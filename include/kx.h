@@ -132,6 +132,25 @@ kx_status kx_step(kx_ctx *ctx, double t, double *const *U);
  * steps `nsteps` times, copies back, synchronises (end-to-end entry point). */
 kx_status kx_integrate_host(kx_ctx *ctx, double t0, int nsteps, double *const *U_host);
 
+/* ---------------------------------------------------------------- multi-GPU -------- */
+/* Slab decomposition along i_d over P ranks (one process per GPU); see DESIGN.md §8.
+ * Every rank calls kx_set_grid with the GLOBAL extents (n_1 and n_d divisible by P, d >= 2),
+ * the same direction matrices, model and tau; its tensors U[c] hold the local slab
+ * i_d in [rank n_d/P, (rank+1) n_d/P) in vec order (N/P doubles).  kx_step then performs the
+ * sharded step with NCCL all-to-all exchanges (ncclSend/ncclRecv groups, fp64) enqueued on the
+ * context stream.  The single-GPU operators (kx_mode_product, kx_tucker, kx_kronsum,
+ * kx_phi_apply, kx_integrate_host) return KX_ERR_UNSUPPORTED on distributed contexts. */
+/* 128-byte ncclUniqueId (NCCL from the process, dlopen'ed); create on rank 0, broadcast. */
+kx_status kx_nccl_unique_id(void *out128);
+kx_status kx_create_dist(kx_ctx **ctx, int device, void *cuda_stream, const void *nccl_unique_id,
+                         int rank, int nranks);
+/* In-process loopback group: nranks contexts on ONE device sharing one stream; the exchanges are
+ * device copies issued between phases by kx_step_group (no kernel ever waits on another rank).
+ * Used to test the sharded schedule on a single GPU.  U holds nranks*ncomp device pointers,
+ * rank-major (U[r*ncomp + c]). */
+kx_status kx_create_group(kx_ctx **ctxs, int nranks, int device, void *cuda_stream);
+kx_status kx_step_group(kx_ctx *const *ctxs, int nranks, double t, double *const *U);
+
 /* ---------------------------------------------------------------- utilities -------- */
 kx_status kx_get_counters(const kx_ctx *ctx, kx_counters *out);
 kx_status kx_reset_counters(kx_ctx *ctx);

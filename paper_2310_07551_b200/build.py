@@ -25,6 +25,20 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
 
 
+def nccl_include() -> str | None:
+    """nccl.h of the NCCL that torch loads (pip wheel nvidia-nccl-cu12), so the process has a
+    single NCCL; the library dlopens libnccl.so.2 at kx_create_dist time."""
+    try:
+        import nvidia.nccl as m
+        for base in list(getattr(m, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return None
+
+
 def nvcc() -> str:
     for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and os.path.exists(cand):
@@ -54,6 +68,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
         if force or _newer(obj, [src] + headers):
             cmd = [nvcc()] + ARCH + COMMON
+            inc = nccl_include()
+            if inc:
+                cmd += ["-I", inc, "-DKX_HAVE_NCCL"]
             if src.endswith(".cu") and verbose:
                 cmd += ["-Xptxas", "-v"]
             cmd += ["-c", src, "-o", obj]

@@ -71,17 +71,59 @@ struct Cfg {
   static_assert(IA <= 32 && IB <= 32, "validity masks are 32-bit");
 };
 
-// Launch schedule.  persistent = 0: one output tile per CTA (grid.x = tiles, grid.y = z).
-// persistent = 1 (hybrid data-parallel + stream-K): grid.x = G co-resident CTAs; tiles
-// [0, dp_tiles) are processed whole, round-robin; the remaining tiles' k-iterations are split
-// into G_sk contiguous ranges.  A CTA whose range starts inside a tile stores its partial
-// accumulators to its workspace slot and raises its flag; the CTA that owns the tile's first
-// k-range adds the later partials in increasing-k order (deterministic), then runs the
-// epilogue.  Waits only go to higher CTA indices, whose partial comes first in their range.
+// Persistent, cross-tile pipelined schedule.  grid.x = G co-resident CTAs.  CTA i walks
+// a work list: data-parallel tiles i, i+G, ... < dp_tiles (whole k range), then its share of
+// the stream-K region (tiles [dp_tiles, T) with their k-iterations split into G_sk contiguous
+// ranges).  The cp.async producer runs STAGES-1 k-tiles ahead of the DMMA consumer ACROSS
+// tile boundaries, so the next tile's first stages load while this tile's epilogue runs.
+// Stream-K fix-up: a CTA whose range starts inside a tile stores its partial accumulators to
+// its workspace slot and raises its flag; the CTA owning the tile's first k-range adds the
+// later partials in increasing-k order (deterministic) and runs the epilogue.  Waits only go
+// to higher CTA indices, whose contribution is the first item of their stream-K range.
 struct Sched {
-  int tiles_m = 1, tiles_n = 1, m_fastest = 0, z0 = 0;
-  int persistent = 0, G = 0, G_sk = 0, ktiles = 0;
+  int tiles_m = 1, tiles_n = 1, m_fastest = 0, ktiles = 0;
+  int G = 1, G_sk = 0;
   long long dp_tiles = 0, sk_units = 0;
+};
+
+struct Seg {
+  long long tl;
+  int kb, ke;
+};
+
+struct WorkIter {
+  long long next_dp, dp_tiles, u, u1;
+  int G, ktiles;
+  __device__ __forceinline__ void init(const Sched& sc, int i) {
+    next_dp = i;
+    dp_tiles = sc.dp_tiles;
+    G = sc.G;
+    ktiles = sc.ktiles;
+    if (i < sc.G_sk) {
+      u = (long long)i * sc.sk_units / sc.G_sk;
+      u1 = (long long)(i + 1) * sc.sk_units / sc.G_sk;
+    } else {
+      u = u1 = 0;
+    }
+  }
+  __device__ __forceinline__ bool next(Seg& s) {
+    if (next_dp < dp_tiles) {
+      s.tl = next_dp;
+      s.kb = 0;
+      s.ke = ktiles;
+      next_dp += G;
+      return true;
+    }
+    if (u < u1) {
+      const long long tr = u / ktiles;
+      s.kb = (int)(u - tr * ktiles);
+      s.ke = (int)((long long)s.kb + (u1 - u) < ktiles ? s.kb + (u1 - u) : ktiles);
+      s.tl = dp_tiles + tr;
+      u += s.ke - s.kb;
+      return true;
+    }
+    return false;
+  }
 };
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
@@ -97,8 +139,9 @@ struct GemmTile {
 
   __device__ __forceinline__ static Coord coords(const GemmArgs& p, const Sched& sc, long long tl) {
     const long long tmn = (long long)sc.tiles_m * sc.tiles_n;
-    const int z = sc.z0 + (int)(tl / tmn);
-    const int r = (int)(tl - (tl / tmn) * tmn);
+    const long long zq = tl / tmn;
+    const int z = (int)zq;
+    const int r = (int)(tl - zq * tmn);
     int tm, tn;
     if (sc.m_fastest) {
       tm = r % sc.tiles_m;
@@ -117,118 +160,81 @@ struct GemmTile {
     return c;
   }
 
-  // acc += sum over k-tiles [kb, ke) of the (m0, n0) tile.
-  __device__ __forceinline__ static void mainloop(const GemmArgs& p, double* smem, const Coord& cd,
-                                                  int kb, int ke, double (&acc)[FM][FN][2]) {
-    double* As = smem;
-    double* Bs = smem + STAGES * A_ST;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g = lane >> 2, t4 = lane & 3;
-    const int wm0 = (warp / C_::WARPS_N) * WM, wn0 = (warp % C_::WARPS_N) * WN;
-    const int m0 = cd.m0, n0 = cd.n0;
-    const double* __restrict__ A = p.A[cd.s] + cd.t * p.sA_t + cd.b * p.sA_b;
-    const double* __restrict__ B = p.B[cd.s] + cd.t * p.sB_t + cd.b * p.sB_b;
-    const int M = p.M, N = p.N, kseg = p.kseg;
-    const int lda = (int)p.lda, ldb = (int)p.ldb;
-    const int kps = (kseg + BK - 1) / BK;
+  // cp.async producer state for one tile: 32-bit offsets inside the operands + validity
+  // masks; per k-tile only a pointer add and a predicate remain.
+  struct Loader {
+    const double* A;
+    const double* B;
+    int offA[IA], offB[IB];
+    unsigned okA, okB;
+    int lseg, lk0;
 
-    // per-thread loader state: 32-bit offsets inside the operand + validity masks; per k-tile
-    // only a pointer add and a predicate remain
-    int offA[IA], krA[IA], offB[IB], krB[IB], smA[IA], smB[IB];
-    unsigned okA = 0, okB = 0;
-#pragma unroll
-    for (int it = 0; it < IA; ++it) {
-      const int c = tid + it * NT;
-      if constexpr (AROW) {
-        const int r = c / CPR_A, kc = (c % CPR_A) * VEC;
-        const bool v = m0 + r < M;
-        offA[it] = (v ? (m0 + r) : 0) * lda + kc;
-        krA[it] = kc;
-        okA |= (unsigned)v << it;
-      } else {
-        const int kr = c / CPR_A, mc = (c % CPR_A) * VEC;
-        const bool v = m0 + mc < M;
-        offA[it] = kr * lda + (v ? m0 + mc : 0);
-        krA[it] = kr;
-        okA |= (unsigned)v << it;
-      }
-      smA[it] = (c / CPR_A) * SA + (c % CPR_A) * VEC;
-    }
-#pragma unroll
-    for (int it = 0; it < IB; ++it) {
-      const int c = tid + it * NT;
-      const int kr = c / CPR_B, nc = (c % CPR_B) * VEC;
-      const bool v = n0 + nc < N;
-      offB[it] = kr * ldb + (v ? n0 + nc : 0);
-      krB[it] = kr;
-      okB |= (unsigned)v << it;
-      smB[it] = (c / CPR_B) * SB + (c % CPR_B) * VEC;
-    }
-
-    int lseg = kb / kps, lk0 = (kb - (kb / kps) * kps) * BK;   // load cursor
-    auto issue_loads = [&](int stage) {
-      double* as = As + stage * A_ST;
-      double* bs = Bs + stage * B_ST;
-      const double* Ab = A + p.seg_off[lseg] + (AROW ? (long long)lk0 : (long long)lk0 * lda);
-      const double* Bb = B + ((long long)lseg * kseg + lk0) * ldb;
+    __device__ __forceinline__ void setup(const GemmArgs& p, const Coord& cd, int kb) {
+      const int tid = threadIdx.x;
+      A = p.A[cd.s] + cd.t * p.sA_t + cd.b * p.sA_b;
+      B = p.B[cd.s] + cd.t * p.sB_t + cd.b * p.sB_b;
+      const int lda = (int)p.lda, ldb = (int)p.ldb;
+      okA = okB = 0;
 #pragma unroll
       for (int it = 0; it < IA; ++it) {
-        const bool v = ((okA >> it) & 1u) && (lk0 + krA[it] < kseg);
-        const double* src = v ? Ab + offA[it] : A;
-        if constexpr (VEC == 2) cp_async16(as + smA[it], src, v);
-        else cp_async8(as + smA[it], src, v);
+        const int c = tid + it * NT;
+        if constexpr (AROW) {
+          const int r = c / CPR_A, kc = (c % CPR_A) * VEC;
+          const bool v = cd.m0 + r < p.M;
+          offA[it] = (v ? (cd.m0 + r) : 0) * lda + kc;
+          okA |= (unsigned)v << it;
+        } else {
+          const int kr = c / CPR_A, mc = (c % CPR_A) * VEC;
+          const bool v = cd.m0 + mc < p.M;
+          offA[it] = kr * lda + (v ? cd.m0 + mc : 0);
+          okA |= (unsigned)v << it;
+        }
       }
 #pragma unroll
       for (int it = 0; it < IB; ++it) {
-        const bool v = ((okB >> it) & 1u) && (lk0 + krB[it] < kseg);
+        const int c = tid + it * NT;
+        const int kr = c / CPR_B, nc = (c % CPR_B) * VEC;
+        const bool v = cd.n0 + nc < p.N;
+        offB[it] = kr * ldb + (v ? cd.n0 + nc : 0);
+        okB |= (unsigned)v << it;
+      }
+      const int kps = (p.kseg + BK - 1) / BK;
+      lseg = kb / kps;
+      lk0 = (kb - lseg * kps) * BK;
+    }
+
+    __device__ __forceinline__ void issue(const GemmArgs& p, double* as, double* bs) {
+      const int tid = threadIdx.x;
+      const int kseg = p.kseg;
+      const double* Ab = A + p.seg_off[lseg] + (AROW ? (long long)lk0 : (long long)lk0 * p.lda);
+      const double* Bb = B + ((long long)lseg * kseg + lk0) * p.ldb;
+#pragma unroll
+      for (int it = 0; it < IA; ++it) {
+        const int c = tid + it * NT;
+        const int kr = AROW ? (c % CPR_A) * VEC : c / CPR_A;
+        const bool v = ((okA >> it) & 1u) && (lk0 + kr < kseg);
+        const double* src = v ? Ab + offA[it] : A;
+        double* dst = as + (c / CPR_A) * SA + (c % CPR_A) * VEC;
+        if constexpr (VEC == 2) cp_async16(dst, src, v);
+        else cp_async8(dst, src, v);
+      }
+#pragma unroll
+      for (int it = 0; it < IB; ++it) {
+        const int c = tid + it * NT;
+        const int kr = c / CPR_B;
+        const bool v = ((okB >> it) & 1u) && (lk0 + kr < kseg);
         const double* src = v ? Bb + offB[it] : B;
-        if constexpr (VEC == 2) cp_async16(bs + smB[it], src, v);
-        else cp_async8(bs + smB[it], src, v);
+        double* dst = bs + kr * SB + (c % CPR_B) * VEC;
+        if constexpr (VEC == 2) cp_async16(dst, src, v);
+        else cp_async8(dst, src, v);
       }
       lk0 += BK;
       if (lk0 >= kseg) {
         lk0 = 0;
         ++lseg;
       }
-    };
-
-    const int n = ke - kb;
-    __syncthreads();   // the previous tile's readers are done with every stage
-#pragma unroll
-    for (int st = 0; st < STAGES - 1; ++st) {
-      if (st < n) issue_loads(st);
-      cp_async_commit();
     }
-    for (int kt = 0; kt < n; ++kt) {
-      cp_async_wait<STAGES - 2>();
-      __syncthreads();
-      const double* as = As + (kt % STAGES) * A_ST;
-      const double* bs = Bs + (kt % STAGES) * B_ST;
-      const int nk = kt + STAGES - 1;
-#pragma unroll
-      for (int kk = 0; kk < BK; kk += 4) {
-        double af[FM], bf[FN];
-#pragma unroll
-        for (int i = 0; i < FM; ++i) {
-          if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
-          else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
-        }
-#pragma unroll
-        for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
-#pragma unroll
-        for (int i = 0; i < FM; ++i)
-#pragma unroll
-          for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-        if (kk == 0) {
-          // prefetch tile kt+STAGES-1 into the stage freed by iteration kt-1, interleaved
-          // with the DMMAs already queued for this k-step
-          if (nk < n) issue_loads(nk % STAGES);
-          cp_async_commit();
-        }
-      }
-    }
-    cp_async_wait<0>();
-  }
+  };
 
   // C = alpha*acc + beta*D + gamma*E + diag*[m==n]
   __device__ __forceinline__ static void epilogue(const GemmArgs& p, const Coord& cd,
@@ -288,58 +294,108 @@ struct GemmTile {
   }
 };
 
-template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool SKP>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT)
     gemm_kernel(const GemmArgs p, const Sched sc) {
   using T_ = GemmTile<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  constexpr int NT = T_::NT, FM = T_::FM, FN = T_::FN;
+  using Coord = typename T_::Coord;
+  constexpr int NT = T_::NT, FM = T_::FM, FN = T_::FN, SA = T_::SA, SB = T_::SB;
+  constexpr int A_ST = T_::A_ST, B_ST = T_::B_ST;
   extern __shared__ __align__(16) double smem[];
-  double acc[FM][FN][2];
-  const int ktiles = sc.ktiles;
-  if constexpr (!SKP) {
-    const long long tl = (long long)blockIdx.y * sc.tiles_m * sc.tiles_n + blockIdx.x;
-    const typename T_::Coord cd = T_::coords(p, sc, tl);
-    T_::zero(acc);
-    T_::mainloop(p, smem, cd, 0, ktiles, acc);
-    T_::epilogue(p, cd, acc);
-    return;
-  } else {
-  const int i = blockIdx.x, G = sc.G;
-  for (long long tl = i; tl < sc.dp_tiles; tl += G) {
-    const typename T_::Coord cd = T_::coords(p, sc, tl);
-    T_::zero(acc);
-    T_::mainloop(p, smem, cd, 0, ktiles, acc);
-    T_::epilogue(p, cd, acc);
+  double* As = smem;
+  double* Bs = smem + STAGES * A_ST;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm0 = (warp / T_::C_::WARPS_N) * WM, wn0 = (warp % T_::C_::WARPS_N) * WN;
+  const int cta = blockIdx.x;
+
+  // ---- producer
+  WorkIter pit;
+  pit.init(sc, cta);
+  Seg ps;
+  bool p_ok = pit.next(ps);
+  int pk = 0;
+  typename T_::Loader ld;
+  if (p_ok) {
+    pk = ps.kb;
+    ld.setup(p, T_::coords(p, sc, ps.tl), ps.kb);
   }
-  const int Gs = sc.G_sk;
-  if (i >= Gs || sc.sk_units == 0) return;
-  const long long u0 = (long long)i * sc.sk_units / Gs, u1 = (long long)(i + 1) * sc.sk_units / Gs;
-  double* ws_me = p.sk_ws + (size_t)i * (FM * FN * 2 * NT);
-  for (long long u = u0; u < u1;) {
-    const long long tr = u / ktiles;
-    const int kb = (int)(u - tr * ktiles);
-    const int ke = (int)((long long)kb + (u1 - u) < ktiles ? kb + (u1 - u) : ktiles);
-    const typename T_::Coord cd = T_::coords(p, sc, sc.dp_tiles + tr);
-    T_::zero(acc);
-    T_::mainloop(p, smem, cd, kb, ke, acc);
-    if (kb > 0) {
-      // contributor: publish the partial (thread-fragment order, coalesced) and signal
+  auto produce = [&](int stage) {
+    if (p_ok) {
+      ld.issue(p, As + stage * A_ST, Bs + stage * B_ST);
+      if (++pk == ps.ke) {
+        p_ok = pit.next(ps);
+        if (p_ok) {
+          pk = ps.kb;
+          ld.setup(p, T_::coords(p, sc, ps.tl), ps.kb);
+        }
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) produce(st);
+
+  // ---- consumer
+  WorkIter cit;
+  cit.init(sc, cta);
+  Seg cs;
+  bool c_ok = cit.next(cs);
+  if (!c_ok) {
+    cp_async_wait<0>();
+    return;
+  }
+  int ck = cs.kb;
+  Coord cd = T_::coords(p, sc, cs.tl);
+  double acc[FM][FN][2];
+  T_::zero(acc);
+  int stage_c = 0, stage_p = STAGES - 1;
+  double* ws_me = p.sk_ws + (size_t)cta * (FM * FN * 2 * NT);
+  while (true) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const double* as = As + stage_c * A_ST;
+    const double* bs = Bs + stage_c * B_ST;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[FM], bf[FN];
+#pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
+        else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+      }
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      if (kk == 0) produce(stage_p);   // overlaps the DMMAs queued for this k-step
+    }
+    stage_c = stage_c + 1 == STAGES ? 0 : stage_c + 1;
+    stage_p = stage_p + 1 == STAGES ? 0 : stage_p + 1;
+    if (++ck < cs.ke) continue;
+
+    // ---- segment finished
+    if (cs.kb > 0) {
+      // stream-K contributor: publish the partial (thread-fragment order, coalesced), signal
 #pragma unroll
       for (int a = 0; a < FM; ++a)
 #pragma unroll
         for (int c = 0; c < FN; ++c)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) __stcg(ws_me + ((a * FN + c) * 2 + e) * NT + threadIdx.x, acc[a][c][e]);
+          for (int e = 0; e < 2; ++e) __stcg(ws_me + ((a * FN + c) * 2 + e) * NT + tid, acc[a][c][e]);
       __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0) atomicExch(p.sk_flags + i, 1);
+      if (tid == 0) atomicExch(p.sk_flags + cta, 1);
     } else {
-      if (ke < ktiles) {
+      if (cs.ke < sc.ktiles) {
         // owner of a split tile: add the later k-ranges' partials in increasing k
-        for (int j = i + 1; j < Gs; ++j) {
-          const long long bj = (long long)j * sc.sk_units / Gs;
-          if (bj >= (tr + 1) * ktiles) break;
-          if (threadIdx.x == 0) {
+        const long long tr = cs.tl - sc.dp_tiles;
+        for (int j = cta + 1; j < sc.G_sk; ++j) {
+          const long long bj = (long long)j * sc.sk_units / sc.G_sk;
+          if (bj >= (tr + 1) * sc.ktiles) break;
+          if (tid == 0) {
             volatile int* f = p.sk_flags + j;
             while (*f == 0) __nanosleep(64);
             __threadfence();
@@ -352,37 +408,45 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
 #pragma unroll
             for (int c = 0; c < FN; ++c)
 #pragma unroll
-              for (int e = 0; e < 2; ++e) acc[a][c][e] += __ldcg(wj + ((a * FN + c) * 2 + e) * NT + threadIdx.x);
+              for (int e = 0; e < 2; ++e) acc[a][c][e] += __ldcg(wj + ((a * FN + c) * 2 + e) * NT + tid);
         }
       }
       T_::epilogue(p, cd, acc);
     }
-    u += ke - kb;
+    if (!cit.next(cs)) break;
+    ck = cs.kb;
+    cd = T_::coords(p, sc, cs.tl);
+    T_::zero(acc);
   }
-  }
+  cp_async_wait<0>();
 }
 
 struct TileChoice {
-  int bm, bn, occ;
+  int bm, bn, bk, occ;
   double eff;
 };
 // Resident CTAs per SM (register/smem-limited) and relative per-SM efficiency of each config.
-constexpr TileChoice kTiles[3] = {{128, 128, 1, 1.00}, {128, 64, 2, 0.97}, {64, 64, 3, 0.90}};
+constexpr TileChoice kTiles[3] = {{128, 128, 32, 1, 1.00}, {128, 64, 16, 2, 0.95}, {64, 64, 16, 3, 0.90}};
+
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
+struct Prepared {
+  static inline bool done = false;
+  static inline int occ = 1;   // resident CTAs per SM (occupancy API)
+};
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
 cudaError_t prepare_cfg() {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, false>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
+  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  if (!P_::done) {
+    auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
     if (e != cudaSuccess) return e;
-    if constexpr (BM == 128 && BN == 128) {
-      e = cudaFuncSetAttribute(gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, true>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
-      if (e != cudaSuccess) return e;
-    }
-    attr_done = true;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C_::NT, C_::SMEM);
+    if (e != cudaSuccess) return e;
+    P_::occ = occ < 1 ? 1 : occ;
+    P_::done = true;
   }
   return cudaSuccess;
 }
@@ -390,9 +454,9 @@ cudaError_t prepare_cfg() {
 int num_sms();
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
-cudaError_t launch_cfg(const GemmArgs& g, int nz, bool allow_sk, cudaStream_t stream) {
+cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, false>;
+  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>();
   if (e != cudaSuccess) return e;
   Sched sc;
@@ -400,39 +464,33 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, bool allow_sk, cudaStream_t st
   sc.tiles_n = (g.N + BN - 1) / BN;
   sc.m_fastest = AROW ? 0 : 1;
   sc.ktiles = ((g.kseg + BK - 1) / BK) * g.nseg;
-  const long long tmn = (long long)sc.tiles_m * sc.tiles_n;
-  const long long T = tmn * nz;
-  const int G = num_sms();   // 1 CTA/SM for the configs that allow stream-K
-  if (allow_sk && g.sk_ws && g.sk_flags && G <= kSkSlots && T % G != 0 && sc.ktiles >= 8) {
-    const double waves = (double)T / G;
-    const double quant = std::ceil(waves) / waves;   // classic-schedule slowdown
-    if (quant > 1.06) {
-      long long dp = (T / G) * G;
-      if (dp >= G && (T - dp) * 2 < G) dp -= G;      // short tail: spread one more wave
-      sc.persistent = 1;
-      sc.G = G;
+  const long long T = (long long)sc.tiles_m * sc.tiles_n * nz;
+  const long long Gmax = (long long)num_sms() * P_::occ;
+  sc.G = (int)std::min<long long>(T, Gmax);
+  sc.dp_tiles = T;
+  const bool sk_ok = g.sk_ws && g.sk_flags && Gmax <= kSkSlots * (128 * 128) / (BM * BN) &&
+                     Gmax <= kSkFlags && sc.ktiles >= 8;
+  if (sk_ok && T % Gmax != 0) {
+    const double waves = (double)T / Gmax;
+    if (std::ceil(waves) / waves > 1.06) {   // classic tail would waste > 6%
+      long long dp = (T / Gmax) * Gmax;
+      if (dp >= Gmax && (T - dp) * 2 < Gmax) dp -= Gmax;   // short tail: spread one more wave
+      sc.G = (int)Gmax;
       sc.dp_tiles = dp;
       sc.sk_units = (T - dp) * sc.ktiles;
-      sc.G_sk = (int)std::min<long long>(G, sc.sk_units / 4);
-      if constexpr (BM == 128 && BN == 128)
-        gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, true><<<dim3(G, 1), C_::NT, C_::SMEM, stream>>>(g, sc);
-      return cudaGetLastError();
+      sc.G_sk = (int)std::min<long long>(Gmax, sc.sk_units / 4);
     }
   }
-  for (int z0 = 0; z0 < nz; z0 += 65535) {
-    sc.z0 = z0;
-    dim3 grid((unsigned)tmn, (unsigned)std::min(65535, nz - z0));
-    kern<<<grid, C_::NT, C_::SMEM, stream>>>(g, sc);
-  }
+  gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc);
   return cudaGetLastError();
 }
 
 template <bool AROW, int VEC>
 cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
   switch (which) {
-    case 0: return launch_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>(g, nz, true, stream);
-    case 1: return launch_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>(g, nz, false, stream);
-    default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, false, stream);
+    case 0: return launch_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>(g, nz, stream);
+    case 1: return launch_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>(g, nz, stream);
+    default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
   }
 }
 
@@ -489,17 +547,18 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
     if (g.D[s]) vec = vec && aligned16(g.D[s]);
     if (g.E[s]) vec = vec && aligned16(g.E[s]);
   }
-  // Tile choice: minimise (waves x per-wave work) / efficiency on 148 SMs.
+  // Tile choice: minimise (waves x per-wave work) / efficiency on the SM count.  With the
+  // stream-K tail (k-tiles >= 8) a partial last wave costs only its fraction (+3% fix-up).
   const int nsm = num_sms();
   int best = 0;
   double best_cost = 1e300;
   for (int i = 0; i < 3; ++i) {
     const TileChoice& c = kTiles[i];
     const double tiles = (double)((g.M + c.bm - 1) / c.bm) * ((g.N + c.bn - 1) / c.bn) * nz;
-    double waves = std::ceil(tiles / ((double)nsm * c.occ));
-    const int kt = (g.kseg + 31) / 32 * g.nseg;
-    if (i == 0 && g.sk_ws && kt >= 8 && waves / (tiles / nsm) > 1.06)
-      waves = 1.03 * tiles / nsm;   // stream-K tail: ~3% fix-up overhead
+    const double slots = (double)nsm * c.occ;
+    double waves = std::ceil(tiles / slots);
+    const int kt = (g.kseg + c.bk - 1) / c.bk * g.nseg;
+    if (kt >= 8 && waves / (tiles / slots) > 1.06) waves = 1.03 * tiles / slots;
     const double cost = waves * c.occ * c.bm * c.bn / c.eff;
     if (cost < best_cost * 0.999) {
       best_cost = cost;

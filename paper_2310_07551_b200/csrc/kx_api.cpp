@@ -4,6 +4,7 @@
 #include "kx.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -14,6 +15,9 @@
 #include <vector>
 
 #include "kx_internal.h"
+#ifdef KX_HAVE_NCCL
+#include <nccl.h>
+#endif
 
 using kx::GemmArgs;
 using kx::MAXS;
@@ -74,8 +78,10 @@ struct kx_ctx {
   std::string err;
 
   int d = 0, ncomp = 0;
-  long long n[KX_MAXD] = {};
+  long long n[KX_MAXD] = {};     // global extents (matrix sizes)
   long long N = 0;
+  long long tn[KX_MAXD] = {};    // extents of the local tensors the current launches act on
+  long long tN = 0;              // (= n, N on one GPU; a slab layout on a distributed context)
   std::vector<std::vector<std::vector<double>>> A_host;   // [c][mu]
   std::vector<std::vector<double*>> A_dev;                 // [c][mu]
   std::vector<std::vector<double*>> A_tri;                 // [c][mu]: lo|di|up (3 n) or null
@@ -123,6 +129,22 @@ struct kx_ctx {
   kx_counters step_delta{};
 
   // profiling
+  // distributed slab decomposition along i_d: dist = 1 NCCL rank,
+  // dist = 2 member of an in-process loopback group (exchanges are device copies)
+  int dist = 0, rank = 0, nranks = 1;
+  void* nccl_comm = nullptr;
+  long long nA[KX_MAXD] = {};    // local extents, layout A: i_d sharded (n_d / P)
+  long long nB[KX_MAXD] = {};    // local extents, layout B: i_1 sharded (n_1 / P)
+  long long Nloc = 0;
+  double* RA[MAXS] = {};         // received term slots, peer-major layout A (nslots x Nloc)
+  double* T1G_pack[MAXS] = {};   // (U x_1 A_1 + G), peer-packed
+  double* U_pack[MAXS] = {};
+  double* T1G_B[MAXS] = {};
+  double* U_B[MAXS] = {};
+  double* F_B[MAXS] = {};
+  double* D_pack[MAXS] = {};
+  double* D_B[MAXS] = {};
+
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   struct Rec { int cls; int e0, e1; double flops; };
@@ -252,12 +274,16 @@ void drop_bank(kx_ctx* c) {
   for (auto& s : c->stages) s = Stage{};
   c->nstages = 0;
   c->bank_ready = false;
-  for (int s = 0; s < MAXS; ++s) c->G[s] = c->F[s] = c->D[s] = c->Us[s] = c->W1[s] = c->W2[s] = nullptr;
+  for (int s = 0; s < MAXS; ++s) {
+    c->G[s] = c->F[s] = c->D[s] = c->Us[s] = c->W1[s] = c->W2[s] = nullptr;
+    c->RA[s] = c->T1G_pack[s] = c->U_pack[s] = c->T1G_B[s] = c->U_B[s] = c->F_B[s] = nullptr;
+    c->D_pack[s] = c->D_B[s] = nullptr;
+  }
 }
 
 long long prod_range(const kx_ctx* c, int lo, int hi) {   // prod_{lo <= mu <= hi} n_mu (1-based)
   long long p = 1;
-  for (int mu = lo; mu <= hi; ++mu) p *= c->n[mu - 1];
+  for (int mu = lo; mu <= hi; ++mu) p *= c->tn[mu - 1];
   return p;
 }
 
@@ -273,7 +299,7 @@ kx_status mode_product_multi(kx_ctx* c, int ns, const double* const* X, double* 
                              int mu, const double* const* L, double alpha, double beta,
                              const double* const* Dd) {
   GemmArgs g;
-  const long long nm = c->n[mu - 1];
+  const long long nm = c->tn[mu - 1];
   const long long R = prod_range(c, 1, mu - 1);     // prod_{nu<mu}
   const long long Bt = prod_range(c, mu + 1, c->d); // prod_{nu>mu}
   g.ns = ns;
@@ -282,7 +308,7 @@ kx_status mode_product_multi(kx_ctx* c, int ns, const double* const* X, double* 
   if (mu == 1) {
     // Y_r = X_r * L^T : A = X (ROW, k contiguous), B = L column-major buffer (row-major L^T)
     g.arow = true;
-    g.M = (int)(c->N / nm);
+    g.M = (int)(c->tN / nm);
     g.N = (int)nm;
     g.kseg = (int)nm;
     g.nseg = 1;
@@ -338,16 +364,16 @@ kx_status kronsum_multi(kx_ctx* c, int comp0, int ns, const double* const* X, do
     kx::StencilArgs a;
     a.d = c->d;
     a.ns = ns;
-    a.N = c->N;
+    a.N = c->tN;
     a.beta = beta;
-    for (int mu = 0; mu < c->d; ++mu) a.n[mu] = c->n[mu];
+    for (int mu = 0; mu < c->d; ++mu) a.n[mu] = c->tn[mu];
     for (int s = 0; s < ns; ++s) {
       a.X[s] = X[s];
       a.Y[s] = Y[s];
       a.Dd[s] = (Dd && beta != 0.0) ? Dd[s] : nullptr;
       for (int mu = 0; mu < c->d; ++mu) {
         const double* t = c->A_tri[comp0 + s][mu];
-        const long long n = c->n[mu];
+        const long long n = c->tn[mu];
         a.lo[s][mu] = t;
         a.di[s][mu] = t + n;
         a.up[s][mu] = t + 2 * n;
@@ -380,12 +406,12 @@ kx_status kronsum_multi(kx_ctx* c, int comp0, int ns, const double* const* X, do
 kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* const* X,
                       int slot, double* const** out_ws) {
   const int d = c->d;
-  const long long N = c->N;
+  const long long N = c->tN;
   const int ns = c->ncomp;
   *out_ws = nullptr;
   if (d == 1) return KX_OK;
   {
-    const long long nd = c->n[d - 1];
+    const long long nd = c->tn[d - 1];
     const long long R = N / nd;
     GemmArgs g;
     g.arow = false;
@@ -406,7 +432,7 @@ kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* c
   double** cur = c->W1;
   double** nxt = c->W2;
   for (int mu = d - 1; mu >= 2; --mu) {
-    const long long nm = c->n[mu - 1];
+    const long long nm = c->tn[mu - 1];
     const long long R = prod_range(c, 1, mu - 1);
     const long long Bt = prod_range(c, mu + 1, d);
     GemmArgs g;
@@ -441,10 +467,10 @@ kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* c
 kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
                            const int* slots, double* const* B, double* const* Y, double alpha,
                            double beta, const double* const* Dd) {
-  const long long n1 = c->n[0];
+  const long long n1 = c->tn[0];
   GemmArgs g;
   g.arow = true;
-  g.M = (int)(c->N / n1);
+  g.M = (int)(c->tN / n1);
   g.N = (int)n1;
   g.kseg = (int)n1;
   g.nseg = nseg;
@@ -455,7 +481,7 @@ kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* sr
   g.ns = c->ncomp;
   g.alpha = alpha;
   g.beta = beta;
-  for (int k = 0; k < nseg; ++k) g.seg_off[k] = ws ? (long long)slots[k] * c->N : 0;
+  for (int k = 0; k < nseg; ++k) g.seg_off[k] = ws ? (long long)slots[k] * c->tN : 0;
   for (int s = 0; s < c->ncomp; ++s) {
     g.A[s] = ws ? ws[s] : src[s];
     g.B[s] = B[s];
@@ -471,7 +497,7 @@ kx_status nonlin(kx_ctx* c, int mode, const double* const* u, double* const* out
   kx::PointwiseArgs a;
   a.model = c->model;
   a.ncomp = c->ncomp;
-  a.N = c->N;
+  a.N = c->tN;
   for (int s = 0; s < c->ncomp; ++s) {
     a.u[s] = u[s];
     a.out[s] = out[s];
@@ -861,7 +887,7 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
   }
   c->groups = groups;
   // workspaces
-  const size_t N = (size_t)c->N;
+  const size_t N = (size_t)c->tN;
   auto wal = [&](double** p, size_t cnt) { return dalloc(c, p, cnt, c->ws_allocs); };
   for (int comp = 0; comp < nc; ++comp) {
     KX_TRY(wal(&c->G[comp], N));
@@ -870,6 +896,16 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
     KX_TRY(wal(&c->Us[comp], N));
     if (d >= 2) KX_TRY(wal(&c->W1[comp], (size_t)c->nslots * N));
     if (d >= 3) KX_TRY(wal(&c->W2[comp], (size_t)c->nslots * N));
+    if (c->dist) {
+      KX_TRY(wal(&c->RA[comp], (size_t)c->nslots * N));
+      KX_TRY(wal(&c->T1G_pack[comp], N));
+      KX_TRY(wal(&c->U_pack[comp], N));
+      KX_TRY(wal(&c->T1G_B[comp], N));
+      KX_TRY(wal(&c->U_B[comp], N));
+      KX_TRY(wal(&c->F_B[comp], N));
+      KX_TRY(wal(&c->D_pack[comp], N));
+      KX_TRY(wal(&c->D_B[comp], N));
+    }
   }
   KX_CUDA(c, cudaStreamSynchronize(c->cur));
   c->bank_ready = true;
@@ -966,6 +1002,284 @@ kx_status step_impl(kx_ctx* c, double* const* U) {
 
 }  // namespace
 
+
+// ============================================================ distributed step ==========
+// Slab decomposition along i_d over P ranks.  Layout A (i_d sharded) is the
+// user layout; layout B (i_1 sharded) holds full i_d fibres.  Per exprk3ds step and component:
+//   [A] G = g(U); (U x_1 A_1 + G) and U peer-packed          -> all-to-all -> layout B
+//   [B] F_B = (U x_1 A_1 + G)_B + sum_{mu=d..2} U_B x_mu A_mu; first (mu = d) and middle modes
+//       of the 3T F-terms                                    -> all-to-all of 3T slots -> A
+//   [A] U2 = U + concat-K over (stage term, source rank) segments — the peer-major receive
+//       layout is absorbed by the K segmentation, no unpack; D = g(U2) - G peer-packed
+//   [B] D2 terms ... [A] U3 ... [B] D3 terms ... [A] U+
+// 4 + 5T all-to-alls per component per step; every mode product runs on full fibres on one
+// rank, so results match one GPU up to the summation order of F (rounding level).
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+#ifdef KX_HAVE_NCCL
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+#endif
+  std::string why;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+#ifdef KX_HAVE_NCCL
+  const char* env = getenv("KX_NCCL_LIB");
+  void* h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    api.why = std::string("dlopen libnccl.so.2 failed: ") + dlerror();
+    return api;
+  }
+  auto sym = [&](const char* n) { return dlsym(h, n); };
+  api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+  api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+  api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+  api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+  api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+  api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+  api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+  api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
+           api.GroupStart && api.GroupEnd && api.GetErrorString;
+  if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+#else
+  api.why = "built without nccl.h";
+#endif
+  return api;
+}
+
+// Buffers one rank exchanges after a phase: for k < nbuf, chunk q (count doubles) of send[k]
+// goes to rank q, which stores it at chunk `rank` of its recv[k].
+struct Exchange {
+  int nbuf = 0;
+  size_t count = 0;
+  const double* send[64];
+  double* recv[64];
+  void add(const double* sb, double* rb) {
+    send[nbuf] = sb;
+    recv[nbuf] = rb;
+    ++nbuf;
+  }
+};
+
+void set_layout(kx_ctx* c, bool B) {
+  for (int mu = 0; mu < KX_MAXD; ++mu) c->tn[mu] = B ? c->nB[mu] : c->nA[mu];
+  c->tN = c->Nloc;
+}
+
+// [A] G = g(U); T1G_pack = (U x_1 A_1 + G) peer-packed; U_pack = U peer-packed
+kx_status dist_f_source(kx_ctx* c, double* const* U, Exchange& x) {
+  set_layout(c, false);
+  const int ns = c->ncomp, P = c->nranks;
+  KX_TRY(nonlin(c, 0, U, c->G));
+  const long long n1 = c->n[0], n1l = n1 / P, M = c->Nloc / n1, chunk = c->Nloc / P;
+  GemmArgs g;
+  g.arow = true;
+  g.M = (int)M;
+  g.N = (int)n1l;
+  g.kseg = (int)n1;
+  g.lda = n1;
+  g.ldb = n1;
+  g.ldc = n1l;
+  g.ldd = n1;
+  g.ns = ns;
+  g.nt = P;                 // one batch per destination rank: columns [q n1l, (q+1) n1l)
+  g.sB_t = n1l;
+  g.sC_t = chunk;
+  g.sD_t = n1l;
+  g.beta = 1.0;
+  for (int s = 0; s < ns; ++s) {
+    g.A[s] = U[s];
+    g.B[s] = c->A_dev[s][0];
+    g.C[s] = c->T1G_pack[s];
+    g.D[s] = c->G[s];
+  }
+  KX_TRY(run_gemm(c, g));
+  c->cnt.mode_products += ns;
+  for (int s = 0; s < ns; ++s)
+    for (int q = 0; q < P; ++q)
+      KX_CUDA(c, cudaMemcpy2DAsync(c->U_pack[s] + q * chunk, n1l * 8, U[s] + q * n1l, n1 * 8,
+                                   n1l * 8, M, cudaMemcpyDeviceToDevice, c->cur));
+  x.count = (size_t)chunk;
+  for (int s = 0; s < ns; ++s) {
+    x.add(c->T1G_pack[s], c->T1G_B[s]);
+    x.add(c->U_pack[s], c->U_B[s]);
+  }
+  return KX_OK;
+}
+
+// [B] F_B = T1G_B + sum_{mu = d..2} U_B x_mu A_mu
+kx_status dist_f_build(kx_ctx* c) {
+  set_layout(c, true);
+  const int ns = c->ncomp;
+  const double* L[MAXS];
+  const double* Ub[MAXS];
+  double* Fb[MAXS];
+  const double* Db[MAXS];
+  for (int mu = c->d; mu >= 2; --mu) {
+    for (int s = 0; s < ns; ++s) {
+      L[s] = c->A_dev[s][mu - 1];
+      Ub[s] = c->U_B[s];
+      Fb[s] = c->F_B[s];
+      Db[s] = mu == c->d ? c->T1G_B[s] : c->F_B[s];
+    }
+    KX_TRY(mode_product_multi(c, ns, Ub, Fb, mu, L, 1.0, 1.0, Db));
+  }
+  c->cnt.kronsum_actions += ns;
+  return KX_OK;
+}
+
+// [B] first + middle modes of group gi on X_B; the term slots go back to layout A
+kx_status dist_group(kx_ctx* c, int gi, double* const* Xb, Exchange& x) {
+  set_layout(c, true);
+  const Group& G = c->groups[gi];
+  double* const* ws = nullptr;
+  KX_TRY(group_modes(c, G, 0, G.nterms, Xb, G.slot0, &ws));
+  x.count = (size_t)(c->Nloc / c->nranks);
+  for (int t = 0; t < G.nterms; ++t)
+    for (int s = 0; s < c->ncomp; ++s)
+      x.add(ws[s] + (long long)(G.slot0 + t) * c->Nloc, c->RA[s] + (long long)(G.slot0 + t) * c->Nloc);
+  return KX_OK;
+}
+
+// [A] out = addend + sum over stage terms and source ranks of RA segments x_1 stacked B
+kx_status dist_stage(kx_ctx* c, const Stage& S, double* const* out, const double* const* addend) {
+  set_layout(c, false);
+  const int P = c->nranks;
+  const long long n1 = c->n[0], n1l = n1 / P;
+  if (S.nseg * P > MAXSEG) return fail(c, KX_ERR_UNSUPPORTED, "too many K segments for this rank count");
+  GemmArgs g;
+  g.arow = true;
+  g.M = (int)(c->Nloc / n1);
+  g.N = (int)n1;
+  g.kseg = (int)n1l;
+  g.nseg = S.nseg * P;
+  g.lda = n1l;
+  g.ldb = n1;
+  g.ldc = n1;
+  g.ldd = n1;
+  g.ns = c->ncomp;
+  g.beta = 1.0;
+  for (int k = 0; k < S.nseg; ++k)
+    for (int q = 0; q < P; ++q)
+      g.seg_off[k * P + q] = (long long)S.slot[k] * c->Nloc + (long long)q * (c->Nloc / P);
+  for (int s = 0; s < c->ncomp; ++s) {
+    g.A[s] = c->RA[s];
+    g.B[s] = S.B[s];
+    g.C[s] = out[s];
+    g.D[s] = addend[s];
+  }
+  KX_TRY(run_gemm(c, g));
+  c->cnt.mode_products += (long long)c->ncomp * S.nseg;
+  return KX_OK;
+}
+
+// [A] D_pack = g(Us) - G, peer-packed
+kx_status dist_d_source(kx_ctx* c, Exchange& x) {
+  set_layout(c, false);
+  kx::PointwiseArgs a;
+  a.model = c->model;
+  a.ncomp = c->ncomp;
+  a.N = c->Nloc;
+  a.pack_n1 = c->n[0];
+  a.pack_n1l = c->n[0] / c->nranks;
+  for (int s = 0; s < c->ncomp; ++s) {
+    a.u[s] = c->Us[s];
+    a.out[s] = c->D_pack[s];
+    a.G[s] = c->G[s];
+  }
+  for (int i = 0; i < 8; ++i) a.p[i] = c->params[i];
+  KX_TRY(run_other(c, [&] { return kx::launch_nonlinearity(a, 1, c->cur); }));
+  x.count = (size_t)(c->Nloc / c->nranks);
+  for (int s = 0; s < c->ncomp; ++s) x.add(c->D_pack[s], c->D_B[s]);
+  return KX_OK;
+}
+
+int dist_phases(const kx_ctx* c) { return c->scheme == KX_ETD3RKDS_REAL ? 7 : 5; }
+
+kx_status dist_phase(kx_ctx* c, double* const* U, int ph, Exchange& x) {
+  x = Exchange{};
+  const bool e3 = c->scheme == KX_ETD3RKDS_REAL;
+  const double* Uc[MAXS];
+  const double* Usc[MAXS];
+  for (int s = 0; s < c->ncomp; ++s) {
+    Uc[s] = U[s];
+    Usc[s] = c->Us[s];
+  }
+  switch (ph) {
+    case 0: return dist_f_source(c, U, x);
+    case 1:
+      KX_TRY(dist_f_build(c));
+      return dist_group(c, 0, c->F_B, x);
+    case 2:
+      KX_TRY(dist_stage(c, c->stages[0], c->Us, Uc));
+      return dist_d_source(c, x);
+    case 3: return dist_group(c, 1, c->D_B, x);
+    case 4:
+      if (!e3) {
+        KX_TRY(dist_stage(c, c->stages[1], U, Usc));
+        c->cnt.tucker_ops += (long long)c->ncomp * 2;
+        return KX_OK;
+      }
+      KX_TRY(dist_stage(c, c->stages[1], c->Us, Uc));
+      return dist_d_source(c, x);
+    case 5: return dist_group(c, 2, c->D_B, x);
+    case 6:
+      KX_TRY(dist_stage(c, c->stages[2], U, Uc));
+      c->cnt.tucker_ops += (long long)c->ncomp * (c->groups[0].nterms + 2 * c->T);
+      return KX_OK;
+  }
+  return fail(c, KX_ERR_INVALID, "bad phase");
+}
+
+kx_status nccl_exchange(kx_ctx* c, const Exchange& x) {
+#ifdef KX_HAVE_NCCL
+  NcclApi& api = nccl();
+  ncclComm_t comm = static_cast<ncclComm_t>(c->nccl_comm);
+  auto chk = [&](ncclResult_t r) -> kx_status {
+    if (r != ncclSuccess) return fail(c, KX_ERR_NCCL, std::string("NCCL: ") + api.GetErrorString(r));
+    return KX_OK;
+  };
+  KX_TRY(chk(api.GroupStart()));
+  for (int k = 0; k < x.nbuf; ++k)
+    for (int q = 0; q < c->nranks; ++q) {
+      KX_TRY(chk(api.Send(x.send[k] + q * x.count, x.count, ncclFloat64, q, comm, c->cur)));
+      KX_TRY(chk(api.Recv(x.recv[k] + q * x.count, x.count, ncclFloat64, q, comm, c->cur)));
+    }
+  KX_TRY(chk(api.GroupEnd()));
+  return KX_OK;
+#else
+  (void)x;
+  return fail(c, KX_ERR_UNSUPPORTED, "built without NCCL");
+#endif
+}
+
+kx_status dist_step_nccl(kx_ctx* c, double* const* U) {
+  c->cur = c->stream;
+  Exchange x;
+  for (int ph = 0; ph < dist_phases(c); ++ph) {
+    KX_TRY(dist_phase(c, U, ph, x));
+    if (x.nbuf) KX_TRY(nccl_exchange(c, x));
+  }
+  c->cnt.steps += 1;
+  return KX_OK;
+}
+
+}  // namespace
+
 namespace kx {
 void gemm_prepare_all();
 }
@@ -1004,8 +1318,8 @@ kx_status kx_create(kx_ctx** out, int device, void* cuda_stream) {
   if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->flag), sizeof(int));
   if (e == cudaSuccess)
     e = cudaMalloc(reinterpret_cast<void**>(&c->sk_ws), sizeof(double) * kx::kSkSlots * 128 * 128);
-  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->sk_flags), sizeof(int) * kx::kSkSlots);
-  if (e == cudaSuccess) e = cudaMemset(c->sk_flags, 0, sizeof(int) * kx::kSkSlots);
+  if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&c->sk_flags), sizeof(int) * kx::kSkFlags);
+  if (e == cudaSuccess) e = cudaMemset(c->sk_flags, 0, sizeof(int) * kx::kSkFlags);
   if (e != cudaSuccess) {
     g_create_error = std::string("context setup: ") + cudaGetErrorString(e);
     delete c;
@@ -1030,6 +1344,9 @@ void kx_destroy(kx_ctx* c) {
   for (int s = 0; s < MAXS; ++s)
     if (c->hostU[s]) cudaFree(c->hostU[s]);
   if (c->flag) cudaFree(c->flag);
+#ifdef KX_HAVE_NCCL
+  if (c->nccl_comm && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
+#endif
   if (c->sk_ws) cudaFree(c->sk_ws);
   if (c->sk_flags) cudaFree(c->sk_flags);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -1072,6 +1389,19 @@ kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
   c->ncomp = ncomp;
   for (int mu = 0; mu < KX_MAXD; ++mu) c->n[mu] = mu < d ? n[mu] : 1;
   c->N = N;
+  for (int mu = 0; mu < KX_MAXD; ++mu) c->tn[mu] = c->n[mu];
+  c->tN = N;
+  if (c->dist) {
+    const int P = c->nranks;
+    if (d < 2 || n[0] % P != 0 || n[d - 1] % P != 0)
+      return fail(c, KX_ERR_INVALID, "distributed grids need d >= 2 and n_1, n_d divisible by the rank count");
+    for (int mu = 0; mu < KX_MAXD; ++mu) c->nA[mu] = c->nB[mu] = c->n[mu];
+    c->nA[d - 1] = n[d - 1] / P;
+    c->nB[0] = n[0] / P;
+    c->Nloc = N / P;
+    for (int mu = 0; mu < KX_MAXD; ++mu) c->tn[mu] = c->nA[mu];
+    c->tN = c->Nloc;
+  }
   c->A_host.assign(ncomp, std::vector<std::vector<double>>(d));
   c->A_dev.assign(ncomp, std::vector<double*>(d, nullptr));
   c->A_tri.assign(ncomp, std::vector<double*>(d, nullptr));
@@ -1168,6 +1498,7 @@ kx_status kx_set_tau(kx_ctx* c, double tau, kx_scheme scheme) {
 kx_status kx_mode_product(kx_ctx* c, const double* X, double* Y, int mu, const double* L,
                           double alpha, double beta) {
   KX_TRY(need_grid(c));
+  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (mu < 1 || mu > c->d)
     return fail(c, KX_ERR_INVALID, "mode " + std::to_string(mu) + " outside 1.." + std::to_string(c->d));
   KX_TRY(check_ptr(c, X, "X"));
@@ -1185,6 +1516,7 @@ kx_status kx_mode_product(kx_ctx* c, const double* X, double* Y, int mu, const d
 kx_status kx_tucker(kx_ctx* c, const double* X, double* Y, const double* const* L, double alpha,
                     double beta) {
   KX_TRY(need_grid(c));
+  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   KX_TRY(check_ptr(c, X, "X"));
   KX_TRY(check_ptr(c, Y, "Y"));
   if (!L) return fail(c, KX_ERR_INVALID, "L is NULL");
@@ -1214,6 +1546,7 @@ kx_status kx_tucker(kx_ctx* c, const double* X, double* Y, const double* const* 
 
 kx_status kx_kronsum(kx_ctx* c, int comp, const double* X, double* Y, double beta) {
   KX_TRY(need_grid(c));
+  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
   for (int mu = 1; mu <= c->d; ++mu)
     if (!c->A_dev[comp][mu - 1])
@@ -1239,6 +1572,7 @@ kx_status kx_set_kronsum_mode(kx_ctx* c, int mode) {
 kx_status kx_phi_apply(kx_ctx* c, int comp, int ell, int stage, const double* X, double* Y,
                        double alpha, double beta) {
   KX_TRY(need_grid(c));
+  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
   if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
   auto it = c->phi.find({ell, stage});
@@ -1294,19 +1628,22 @@ kx_status kx_step(kx_ctx* c, double t, double* const* U) {
     for (int r = 0; r < s; ++r)
       if (U[r] == U[s]) return fail(c, KX_ERR_INVALID, "U components must be distinct");
   }
+  if (c->dist == 2) return fail(c, KX_ERR_INVALID, "loopback group members step through kx_step_group");
+  if (c->dist == 1) return dist_step_nccl(c, U);
   return step_impl(c, U);
 }
 
 kx_status kx_integrate_host(kx_ctx* c, double t0, int nsteps, double* const* U_host) {
   KX_TRY(need_grid(c));
+  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
   if (!U_host || nsteps < 0) return fail(c, KX_ERR_INVALID, "bad arguments");
-  const size_t bytes = (size_t)c->N * 8;
+  const size_t bytes = (size_t)c->tN * 8;
   for (int s = 0; s < c->ncomp; ++s) {
     if (!U_host[s]) return fail(c, KX_ERR_INVALID, "U_host[c] is NULL");
     if (!c->hostU[s]) {
       std::vector<double*> keep;
-      KX_TRY(dalloc(c, &c->hostU[s], (size_t)c->N, keep));
+      KX_TRY(dalloc(c, &c->hostU[s], (size_t)c->tN, keep));
     }
     KX_CUDA(c, cudaMemcpyAsync(c->hostU[s], U_host[s], bytes, cudaMemcpyHostToDevice, c->stream));
   }
@@ -1345,7 +1682,7 @@ kx_status kx_check_finite(kx_ctx* c, const double* X) {
   KX_TRY(check_ptr(c, X, "X"));
   int h = 0;
   KX_CUDA(c, cudaMemsetAsync(c->flag, 0, sizeof(int), c->stream));
-  KX_CUDA(c, kx::launch_check_finite(X, c->N, c->flag, c->stream));
+  KX_CUDA(c, kx::launch_check_finite(X, c->tN, c->flag, c->stream));
   KX_CUDA(c, cudaMemcpyAsync(&h, c->flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   KX_CUDA(c, cudaStreamSynchronize(c->stream));
   if (h) return fail(c, KX_ERR_NUMERIC, "non-finite values in tensor");
@@ -1397,6 +1734,108 @@ kx_status kx_get_phi_matrix(kx_ctx* c, int comp, int ell, int stage, int term, i
     KX_CUDA(c, cudaMemcpy(out_host, G.mid[comp][mu - 1] + t * nm * nm, nm * nm * 8,
                           cudaMemcpyDeviceToHost));
   }
+  return KX_OK;
+}
+
+kx_status kx_nccl_unique_id(void* out) {
+  if (!out) return KX_ERR_INVALID;
+#ifdef KX_HAVE_NCCL
+  NcclApi& api = nccl();
+  if (!api.ok) {
+    g_create_error = api.why;
+    return KX_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return KX_ERR_NCCL;
+  std::memcpy(out, &id, sizeof(id));
+  return KX_OK;
+#else
+  g_create_error = "built without NCCL";
+  return KX_ERR_UNSUPPORTED;
+#endif
+}
+
+kx_status kx_create_dist(kx_ctx** out, int device, void* cuda_stream, const void* nccl_unique_id,
+                         int rank, int nranks) {
+  if (!out || !nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks) return KX_ERR_INVALID;
+  KX_TRY(kx_create(out, device, cuda_stream));
+  kx_ctx* c = *out;
+#ifdef KX_HAVE_NCCL
+  NcclApi& api = nccl();
+  if (!api.ok) {
+    g_create_error = api.why;
+    kx_destroy(c);
+    *out = nullptr;
+    return KX_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  ncclResult_t r = api.CommInitRank(&comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    g_create_error = std::string("ncclCommInitRank: ") + api.GetErrorString(r);
+    kx_destroy(c);
+    *out = nullptr;
+    return KX_ERR_NCCL;
+  }
+  c->nccl_comm = comm;
+  c->dist = 1;
+  c->rank = rank;
+  c->nranks = nranks;
+  return KX_OK;
+#else
+  (void)rank;
+  (void)nranks;
+  kx_destroy(c);
+  *out = nullptr;
+  g_create_error = "built without NCCL";
+  return KX_ERR_UNSUPPORTED;
+#endif
+}
+
+kx_status kx_create_group(kx_ctx** ctxs, int nranks, int device, void* cuda_stream) {
+  if (!ctxs || nranks < 1) return KX_ERR_INVALID;
+  for (int r = 0; r < nranks; ++r) ctxs[r] = nullptr;
+  for (int r = 0; r < nranks; ++r) {
+    kx_status st = kx_create(&ctxs[r], device, cuda_stream);
+    if (st != KX_OK) {
+      for (int q = 0; q < r; ++q) kx_destroy(ctxs[q]);
+      return st;
+    }
+    ctxs[r]->dist = 2;
+    ctxs[r]->rank = r;
+    ctxs[r]->nranks = nranks;
+  }
+  return KX_OK;
+}
+
+kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const* U) {
+  (void)t;
+  if (!ctxs || !U || nranks < 1) return KX_ERR_INVALID;
+  for (int r = 0; r < nranks; ++r) {
+    kx_ctx* c = ctxs[r];
+    if (!c || c->dist != 2 || c->rank != r || c->nranks != nranks) return KX_ERR_INVALID;
+    KX_TRY(need_grid(c));
+    if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
+    if (c->scheme != ctxs[0]->scheme || c->N != ctxs[0]->N || c->ncomp != ctxs[0]->ncomp ||
+        c->stream != ctxs[0]->stream)
+      return fail(c, KX_ERR_INVALID, "group members differ in scheme, grid or stream");
+    c->cur = c->stream;
+  }
+  const int nc = ctxs[0]->ncomp;
+  std::vector<Exchange> xs(nranks);
+  for (int ph = 0; ph < dist_phases(ctxs[0]); ++ph) {
+    for (int r = 0; r < nranks; ++r) KX_TRY(dist_phase(ctxs[r], U + (size_t)r * nc, ph, xs[r]));
+    // loopback all-to-all: device copies on the shared stream, after every rank's phase
+    for (int r = 0; r < nranks; ++r) {
+      const Exchange& xr = xs[r];
+      for (int k = 0; k < xr.nbuf; ++k)
+        for (int q = 0; q < nranks; ++q)
+          KX_CUDA(ctxs[r], cudaMemcpyAsync(xs[q].recv[k] + (size_t)r * xr.count, xr.send[k] + (size_t)q * xr.count,
+                                           xr.count * 8, cudaMemcpyDeviceToDevice, ctxs[r]->stream));
+    }
+  }
+  for (int r = 0; r < nranks; ++r) ctxs[r]->cnt.steps += 1;
   return KX_OK;
 }
 

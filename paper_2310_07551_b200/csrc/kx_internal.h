@@ -6,7 +6,7 @@
 namespace kx {
 
 constexpr int MAXS = 4;        // components (species) batched in one launch
-constexpr int MAXSEG = 8;      // K segments of a concatenated-K last-mode product
+constexpr int MAXSEG = 64;     // K segments of a concatenated-K last-mode product (terms x ranks)
 
 // One launch of the mode-product GEMM (kernel K*1):
 //   for z in [0, nz):  s = z / (nt*nb), t = (z / nb) % nt, b = z % nb
@@ -35,7 +35,8 @@ struct GemmArgs {
   double* sk_ws = nullptr;
   int* sk_flags = nullptr;
 };
-constexpr int kSkSlots = 160;   // >= SM count (148)
+constexpr int kSkSlots = 160;    // partial-tile slots of 128x128 doubles (>= SM count)
+constexpr int kSkFlags = 1024;   // flags (>= resident CTAs of any config)
 
 // Launch on `stream`; returns cudaSuccess or the launch error.  Chooses tile config.
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);
@@ -54,6 +55,9 @@ struct PointwiseArgs {
   const double* G[MAXS] = {};
   double* out[MAXS] = {};
   double p[8] = {};
+  // optional peer-packed output (distributed contexts): point (row, i1) of a row-major
+  // (N/n1) x n1 slab goes to out[q*(N/P) + row*n1l + i1 - q*n1l], q = i1 / n1l, n1l = n1/P
+  long long pack_n1 = 0, pack_n1l = 0;
 };
 cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t stream);
 

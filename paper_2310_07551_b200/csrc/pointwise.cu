@@ -28,6 +28,13 @@ __device__ __forceinline__ void g_point(int model, const double* p, double u, do
   }
 }
 
+__device__ __forceinline__ long long out_index(const PointwiseArgs& a, long long p) {
+  if (a.pack_n1l == 0) return p;
+  const long long row = p / a.pack_n1, i1 = p - row * a.pack_n1;
+  const long long q = i1 / a.pack_n1l;
+  return q * (a.N / a.pack_n1 * a.pack_n1l) + row * a.pack_n1l + (i1 - q * a.pack_n1l);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) nonlin2_kernel(const PointwiseArgs a) {
   // two components, vectorised by 2 points (N even)
@@ -51,8 +58,9 @@ __global__ void __launch_bounds__(256) nonlin2_kernel(const PointwiseArgs a) {
       r2.x -= h2.x;
       r2.y -= h2.y;
     }
-    o1[i] = r1;
-    o2[i] = r2;
+    const long long oi = out_index(a, 2 * i) / 2;   // pairs never straddle a peer block
+    o1[oi] = r1;
+    o2[oi] = r2;
   }
 }
 
@@ -67,10 +75,12 @@ __global__ void __launch_bounds__(256) nonlin_scalar_kernel(const PointwiseArgs 
         r1 -= a.G[0][i];
         r2 -= a.G[1][i];
       }
-      a.out[0][i] = r1;
-      a.out[1][i] = r2;
+      const long long oi = out_index(a, i);
+      a.out[0][oi] = r1;
+      a.out[1][oi] = r2;
     } else {
-      for (int c = 0; c < a.ncomp; ++c) a.out[c][i] = MODE == 1 ? -a.G[c][i] : 0.0;   // g = 0 (KX_MODEL_NONE)
+      const long long oi = out_index(a, i);
+      for (int c = 0; c < a.ncomp; ++c) a.out[c][oi] = MODE == 1 ? -a.G[c][i] : 0.0;   // g = 0 (KX_MODEL_NONE)
     }
   }
 }
@@ -182,7 +192,7 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t stream) {
   if (a.N <= 0) return cudaSuccess;
   bool vec = a.ncomp == 2 && a.N % 2 == 0 && al16(a.u[0]) && al16(a.u[1]) && al16(a.out[0]) &&
-             al16(a.out[1]);
+             al16(a.out[1]) && (a.pack_n1l == 0 || a.pack_n1l % 2 == 0);
   if (mode == 1) vec = vec && al16(a.G[0]) && al16(a.G[1]);
   if (vec) {
     const int grid = grid_for(a.N / 2, 256);

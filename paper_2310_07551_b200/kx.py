@@ -62,6 +62,10 @@ _SIGS = {
     "kx_phi_apply": (_i, [_vp, _i, _i, _i, _vp, _vp, _d, _d]),
     "kx_step": (_i, [_vp, _d, C.POINTER(_vp)]),
     "kx_integrate_host": (_i, [_vp, _d, _i, C.POINTER(_vp)]),
+    "kx_nccl_unique_id": (_i, [_vp]),
+    "kx_create_dist": (_i, [C.POINTER(_vp), _i, _vp, _vp, _i, _i]),
+    "kx_create_group": (_i, [C.POINTER(_vp), _i, _i, _vp]),
+    "kx_step_group": (_i, [C.POINTER(_vp), _i, _d, C.POINTER(_vp)]),
     "kx_get_counters": (_i, [_vp, C.POINTER(kx_counters)]),
     "kx_reset_counters": (_i, [_vp]),
     "kx_sync": (_i, [_vp]),
@@ -107,18 +111,38 @@ def scheme_coefficients(scheme: str | int, ell: int, d: int):
     return (list(eta[:n]), list(inner[:n]), [list(alpha[i * d:(i + 1) * d]) for i in range(n)])
 
 
-class Context:
-    """Owns one kx_ctx.  Methods mirror the C ABI one to one."""
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = kx_nccl_unique_id(buf)
+    if st != KX_OK:
+        raise KxError(st, kx_create_error().decode())
+    return buf.raw
 
-    def __init__(self, device: int = 0, stream=None):
+
+class Context:
+    """Owns one kx_ctx.  Methods mirror the C ABI one to one.
+
+    Context(device)                         single GPU
+    Context(device, dist=(uid, rank, P))    one rank of a slab-sharded run (NCCL)
+    """
+
+    def __init__(self, device: int = 0, stream=None, dist=None, handle=None):
         import torch
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
-        h = C.c_void_p()
-        st = kx_create(C.byref(h), device, C.c_void_p(stream.cuda_stream))
-        if st != KX_OK:
-            raise KxError(st, kx_create_error().decode())
+        if handle is not None:
+            h = handle
+        else:
+            h = C.c_void_p()
+            if dist is None:
+                st = kx_create(C.byref(h), device, C.c_void_p(stream.cuda_stream))
+            else:
+                uid, rank, nranks = dist
+                st = kx_create_dist(C.byref(h), device, C.c_void_p(stream.cuda_stream),
+                                    C.c_char_p(uid), rank, nranks)
+            if st != KX_OK:
+                raise KxError(st, kx_create_error().decode())
         self.h = h
         self.d = 0
         self.n: list[int] = []
@@ -228,3 +252,32 @@ class Context:
         self._check(kx_get_phi_matrix(self.h, comp, ell, stage, term, mu,
                                       out.ctypes.data_as(C.POINTER(C.c_double))))
         return out.reshape(n, n, order="F")
+
+
+class Group:
+    """In-process loopback group of `nranks` contexts on one GPU (kx_create_group): the
+    sharded schedule with device-copy exchanges, for single-GPU testing of the multi-GPU path."""
+
+    def __init__(self, nranks: int, device: int = 0, stream=None):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        arr = (C.c_void_p * nranks)()
+        st = kx_create_group(arr, nranks, device, C.c_void_p(stream.cuda_stream))
+        if st != KX_OK:
+            raise KxError(st, kx_create_error().decode())
+        self.nranks = nranks
+        self._arr = arr
+        self.ctx = [Context(device, stream, handle=C.c_void_p(arr[r])) for r in range(nranks)]
+
+    def step(self, U: list[list], t: float = 0.0):
+        """U[r][c]: device slab of component c on rank r."""
+        flat = [_ptr(u) for Ur in U for u in Ur]
+        arr = (C.c_void_p * len(flat))(*flat)
+        st = kx_step_group(self._arr, self.nranks, t, arr)
+        if st != KX_OK:
+            raise KxError(st, kx_last_error(self.ctx[0].h).decode())
+
+    def close(self):
+        for c in self.ctx:
+            c.close()

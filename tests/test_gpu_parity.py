@@ -334,3 +334,50 @@ def test_streamk_shapes_parity_and_determinism(ctx, n):
         ref = vec(mode_product(Xo, L, mu))
         assert relerr(Y1.cpu().numpy(), ref) <= 1e-13, mu
         assert torch.equal(Y1, Y2)
+
+
+def slab(u, n, r, P):
+    """Rank r's slab (i_d in its block) of a vec-order global tensor, as vec-order flat."""
+    T = unvec(u, n)
+    nd = n[-1] // P
+    return vec(T[..., r * nd:(r + 1) * nd])
+
+
+@pytest.mark.parametrize("case", [("schnakenberg", 2, [64, 64], "etd3rkds", 2.0 / 6000, 2),
+                                  ("schnakenberg", 2, [48, 40], "etd3rkds", 1e-4, 4),
+                                  ("fhn", 3, [24, 20, 32], "etd3rkds", 0.015, 2),
+                                  ("fhn", 3, [16, 16, 16], "etd3rkds", 0.015, 4),
+                                  ("schnakenberg", 2, [64, 64], "etd2rkds", 0.25 / 3000, 4),
+                                  ("fhn", 3, [16, 12, 8], "etd2rkds", 0.01, 2)])
+def test_sharded_step_loopback(kx, case):
+    """The slab-sharded schedule (layouts A/B, peer-packed all-to-alls, concat-K over
+    (term, source rank) segments) on an in-process loopback group: equals the single-GPU step
+    to rounding and the oracle to 1e-10."""
+    model, d, n, scheme, tau, P = case
+    prob = inputs.make_problem(model, d, n, seed=5)
+    one = kx.Context(0)
+    setup_problem(one, prob, scheme, tau)
+    U1 = [dev(u) for u in prob.U0]
+    grp = kx.Group(P)
+    for c in grp.ctx:
+        setup_problem(c, prob, scheme, tau)
+    Ug = [[dev(slab(prob.U0[s], n, r, P)) for s in range(2)] for r in range(P)]
+    steps = 3
+    for k in range(steps):
+        one.step(U1)
+        grp.step(Ug)
+    one.sync()
+    grp.ctx[0].sync()
+    ref, _ = integrate(prob, scheme, T=tau * 100, m=100, steps=steps)
+    for s in range(2):
+        u1 = U1[s].cpu().numpy()
+        # assemble the global tensor from the slabs
+        parts = [unvec(Ug[r][s].cpu().numpy(), n[:-1] + [n[-1] // P]) for r in range(P)]
+        ug = vec(np.concatenate(parts, axis=-1))
+        assert relerr(ug, u1) <= 1e-13
+        assert relerr(ug, ref[s]) <= 1e-10
+    cnt = grp.ctx[1].counters()
+    per = 2 if scheme == "etd2rkds" else (10 if d == 2 else 15)
+    assert cnt["tucker_ops"] == steps * 2 * per and cnt["steps"] == steps
+    grp.close()
+    one.close()
