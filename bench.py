@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--no-extras", action="store_true", help="skip Tucker sweep / e2e / cpu leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "sharded"],
+                    help="N>1: replicas (independent problems, weak scaling) or slab-sharded "
+                         "(one global problem, NCCL all-to-all, strong scaling); auto = sharded "
+                         "for the 3D configs, replicas for the 2D ones")
     return ap.parse_args()
 
 
@@ -231,7 +235,7 @@ def tucker_sweep(kx, torch, stream, budget_s=25.0):
     return out
 
 
-def run_kx(args, rank, world):
+def run_kx(args, rank, world, sharded):
     import torch
     import inputs
     from paper_2310_07551_b200 import kx
@@ -239,19 +243,35 @@ def run_kx(args, rank, world):
     torch.cuda.set_device(rank % torch.cuda.device_count())
     stream = torch.cuda.Stream()
     cfg = config_dict(args.config)
-    prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=rank)
     tau = cfg["T"] / cfg["m"]
-    ctx, phi_s = setup_ctx(kx, prob, cfg["scheme"], tau, stream)
-    U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
-    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")   # 256 MiB
-    torch.cuda.synchronize()
-    # warm-up (graph capture + replay)
-    for k in range(args.warmup):
-        ctx.step(U, k * tau)
-    ctx.sync()
     dist = None
     if world > 1:
         import torch.distributed as dist
+    if sharded:
+        uid = [kx.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0, slab=(rank, world))
+        ctx = kx.Context(torch.cuda.current_device(), stream, dist=(uid[0], rank, world))
+        ctx.set_grid(prob.n, 2)
+        for c in range(2):
+            for mu in range(prob.d):
+                ctx.set_direction_matrix(c, mu + 1, prob.A[c][mu])
+        ctx.set_model(prob.model, prob.params)
+        t0 = time.perf_counter()
+        ctx.set_tau(tau, cfg["scheme"])
+        phi_s = time.perf_counter() - t0
+    else:
+        prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=rank)
+        ctx, phi_s = setup_ctx(kx, prob, cfg["scheme"], tau, stream)
+    U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")   # 256 MiB
+    torch.cuda.synchronize()
+    # warm-up (graph capture + replay on one GPU)
+    for k in range(args.warmup):
+        ctx.step(U, k * tau)
+    ctx.sync()
+    if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ctx.reset_counters()
@@ -281,21 +301,37 @@ def run_kx(args, rank, world):
         ms = float(t.item())
     ok = all(ctx.check_finite(u) for u in U)
     res = dict(ms=ms, step_ms=step_ms, prof=prof, cnt=cnt, clocks=clk, phi_s=phi_s, finite=ok)
-    # ---- e2e through kx_integrate_host with pinned host buffers
+    # ---- e2e: pinned host state -> device, one step through the public API, device -> host
     if not args.no_extras:
         Uh = [torch.from_numpy(u.copy()).pin_memory() for u in prob.U0]
-        ctx.integrate_host([u.numpy() for u in Uh], 1)          # warm (graph for hostU)
         e2e_ms = []
-        for k in range(args.steps):
+        for k in range(args.steps + 1):
             flush.fill_(float(k))
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            ctx.integrate_host([u.numpy() for u in Uh], 1)
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        res["e2e_ms"] = sum(e2e_ms) / len(e2e_ms)
-        res["e2e_bytes"] = 2 * prob.N * 8
+            if sharded:
+                with torch.cuda.stream(stream):
+                    for c in range(2):
+                        U[c].copy_(Uh[c], non_blocking=True)
+                    ctx.step(U)
+                    for c in range(2):
+                        Uh[c].copy_(U[c], non_blocking=True)
+                stream.synchronize()
+            else:
+                ctx.integrate_host([u.numpy() for u in Uh], 1)
+            if k > 0:    # the first call captures the graph for the host-path buffers
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e = sum(e2e_ms) / len(e2e_ms)
+        if world > 1:
+            t = torch.tensor([e], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e = float(t.item())
+        res["e2e_ms"] = e
+        res["e2e_bytes"] = 2 * (prob.N // (world if sharded else 1)) * 8
     ctx.close()
-    if not args.no_extras and rank == 0:
+    if not args.no_extras and rank == 0 and not sharded:
         del U, flush
         torch.cuda.empty_cache()
         res["tucker"] = tucker_sweep(kx, torch, stream)
@@ -341,13 +377,14 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
         dist.init_process_group("nccl")
-    res, cfg, prob = run_kx(args, rank, world)
+    sharded = args.mode == "sharded" or (world > 1 and args.mode == "auto" and cfg["d"] == 3)
+    res, cfg, prob = run_kx(args, rank, world, sharded)
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
         return 0
-    value = world * 1e3 / res["ms"]
+    value = (1 if sharded else world) * 1e3 / res["ms"]
     prof = res["prof"]
     peak, hbm = load_peak()
     achieved = prof["gemm_flops"] / prof["gemm_ms"] / 1e9 if prof["gemm_ms"] > 0 else None
@@ -358,11 +395,13 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms"],
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded SplitMix64 initial data, FD Neumann Laplacians; inputs/)",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "grid": prob.n, "species": 2,
                    "scheme": cfg["scheme"], "tau": cfg["T"] / cfg["m"],
-                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "parallelism": (f"slab-sharded x{world} along i_d (NCCL all-to-all)" if sharded
+                                   else ("replicas" if world > 1 else "single GPU")),
                    "l2": "256 MiB buffer written between timed steps (L2 flushed)"},
         "roofline": {"bound": "tensor", "kernel": "mode-product GEMM (fp64 DMMA mma.sync.m8n8k4)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -380,13 +419,13 @@ def main():
         "finite": res["finite"],
     }
     if "e2e_ms" in res:
-        line["e2e"] = {"value": 1e3 / res["e2e_ms"], "unit": "steps/s",
+        line["e2e"] = {"value": (1 if sharded else world) * 1e3 / res["e2e_ms"], "unit": "steps/s",
                        "h2d_bytes_per_step": res["e2e_bytes"], "d2h_bytes_per_step": res["e2e_bytes"]}
     if "tucker" in res:
         line["tucker_tflops"] = res["tucker"]
         if peak:
             line["tucker_frac_of_dmma"] = {k: round(v / peak, 3) for k, v in res["tucker"].items()}
-    if not args.no_extras:
+    if not args.no_extras and prob.N <= 64 * 1024 * 1024:
         v, cores, sample = oracle_sample(args.config, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
                                 "sample": sample}

@@ -133,13 +133,15 @@ class Problem:
 
 
 def make_problem(model: str, d: int, n: int | list[int], seed: int = 0,
-                 amplitude: float | None = None) -> Problem:
+                 amplitude: float | None = None, slab: tuple[int, int] | None = None) -> Problem:
     """Build the Sec. 3 problem with the initial-data recipe of DESIGN.md (R6).
 
     Schnakenberg: Omega = (0,1)^d, u0 = u_e + 1e-5 U(0,1),
     v0 = v_e + 1e-5 U(0,1), (u_e, v_e) = (a^u + a^v, a^v/(a^u+a^v)^2).
     FitzHugh-Nagumo (l.1497-1518): Omega = (0,pi)^d, u0, v0 = 1e-3 U(0,1).
     Stream 0 -> u, stream 1 -> v.
+    slab=(r, P): only rank r's i_d-slab of the initial data (a contiguous vec-order range,
+    produced by the counter-based generator without generating the rest).
     """
     ns = [n] * d if isinstance(n, int) else list(n)
     assert len(ns) == d
@@ -160,7 +162,12 @@ def make_problem(model: str, d: int, n: int | list[int], seed: int = 0,
         raise ValueError(model)
     deltas = (p["du"], p["dv"])
     A = [[laplacian_neumann(nm, length, deltas[c]) for nm in ns] for c in range(2)]
-    U0 = [base[c] + amp * uniform01(seed, c, N) for c in range(2)]
+    if slab is None:
+        U0 = [base[c] + amp * uniform01(seed, c, N) for c in range(2)]
+    else:
+        r, P = slab
+        cnt = N // P
+        U0 = [base[c] + amp * uniform01_range(seed, c, r * cnt, cnt) for c in range(2)]
     return Problem(model=model, d=d, n=ns, length=length, params=p, A=A, U0=U0)
 
 

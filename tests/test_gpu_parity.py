@@ -381,3 +381,28 @@ def test_sharded_step_loopback(kx, case):
     assert cnt["tucker_ops"] == steps * 2 * per and cnt["steps"] == steps
     grp.close()
     one.close()
+
+
+def test_nccl_single_rank_dist_context(kx):
+    """kx_create_dist with one rank (NCCL self-exchange): the distributed code path end to
+    end through NCCL on one GPU, equal to the single-GPU step to rounding."""
+    prob = inputs.make_problem("fhn", 3, [16, 12, 8], seed=7)
+    tau = 0.015
+    uid = kx.nccl_unique_id()
+    dctx = kx.Context(0, dist=(uid, 0, 1))
+    setup_problem(dctx, prob, "etd3rkds", tau)
+    one = kx.Context(0)
+    setup_problem(one, prob, "etd3rkds", tau)
+    Ud = [dev(u) for u in prob.U0]
+    U1 = [dev(u) for u in prob.U0]
+    for _ in range(3):
+        dctx.step(Ud)
+        one.step(U1)
+    dctx.sync()
+    one.sync()
+    for s in range(2):
+        assert relerr(Ud[s].cpu().numpy(), U1[s].cpu().numpy()) <= 1e-13
+    with pytest.raises(kx.KxError, match="distributed"):
+        dctx.tucker(Ud[0], U1[0], [dmat(np.eye(m)) for m in prob.n])
+    dctx.close()
+    one.close()
