@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--no-extras", action="store_true", help="skip Tucker sweep / e2e / cpu leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--scheme", default=None, choices=["etd2rkds", "etd3rkds", "exprk3ds_cplx"],
+                    help="override the config's scheme (e.g. the complex split, Table 2)")
     ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "sharded"],
                     help="N>1: replicas (independent problems, weak scaling) or slab-sharded "
                          "(one global problem, NCCL all-to-all, strong scaling); auto = sharded "
@@ -53,9 +55,14 @@ def parse():
     return ap.parse_args()
 
 
+SCHEME_OVERRIDE = None
+
+
 def config_dict(name):
     import inputs
     cfg = dict(inputs.CONFIGS[name])
+    if SCHEME_OVERRIDE:
+        cfg["scheme"] = SCHEME_OVERRIDE
     return cfg
 
 
@@ -339,7 +346,9 @@ def run_kx(args, rank, world, sharded):
 
 
 def main():
+    global SCHEME_OVERRIDE
     args = parse()
+    SCHEME_OVERRIDE = args.scheme
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus > 1 and world == 1:

@@ -52,7 +52,9 @@ typedef enum {
 
 typedef enum {
   KX_ETD2RKDS = 1,         /* second-order split ETD2RK, any d >= 1            */
-  KX_ETD3RKDS_REAL = 2     /* exprk3ds_real: Table 1 (d = 2) / Table 3 (d >= 3)          */
+  KX_ETD3RKDS_REAL = 2,    /* exprk3ds_real: Table 1 (d = 2) / Table 3 (d >= 3)          */
+  KX_ETD3RKDS_CPLX = 3     /* exprk3ds_cplx: Algorithm 1 with Table 2 (complex, any d >= 2);
+                              the real part is kept after each stage combination (R19)     */
 } kx_scheme;
 
 typedef enum {
@@ -117,7 +119,8 @@ kx_status kx_kronsum(kx_ctx *ctx, int comp, const double *X, double *Y, double b
  * Laplacians of Sec. 3) — the dense mode products would only add exact zeros —
  * and d dense mode products otherwise; mode 1 always uses the dense mode products. */
 kx_status kx_set_kronsum_mode(kx_ctx *ctx, int mode);
-/* Split phi-action from the current bank: Y = alpha * S[X] + beta * Y where
+/* Split phi-action from the current bank: Y = alpha * S[X] + beta * Y (for KX_ETD3RKDS_CPLX
+ * the real part of S[X]) where
  *   S[X] = sum_i eta_i T(X, {phi_{l_i}(c tau alpha_{i,mu} A^comp_mu)}_mu)
  * (eq:split2d / eq:splitnd3 via eq:krontomu).  ETD3RKDS bank: ell in {1,2},
  * stage 0: c = 1/3 (ell = 1 only), stage 1: c = 2/3, stage 2: c = 1.
@@ -165,7 +168,8 @@ kx_status kx_set_profiling(kx_ctx *ctx, int on);
 kx_status kx_get_profile(kx_ctx *ctx, double *gemm_ms, double *other_ms, long long *gemm_launches,
                          long long *other_launches, double *gemm_flops);
 /* Copy one phi-matrix of the current bank to the host (column-major n_mu x n_mu, unscaled):
- * phi_{l_term}(c tau alpha_{term,mu} A^comp_mu) for (ell, stage) as in kx_phi_apply. */
+ * phi_{l_term}(c tau alpha_{term,mu} A^comp_mu) for (ell, stage) as in kx_phi_apply.  For
+ * KX_ETD3RKDS_CPLX, `term` indexes real planes: 2i = Re, 2i+1 = Im of term i. */
 kx_status kx_get_phi_matrix(kx_ctx *ctx, int comp, int ell, int stage, int term, int mu,
                             double *out_host);
 
@@ -175,6 +179,9 @@ kx_status kx_get_phi_matrix(kx_ctx *ctx, int comp, int ell, int stage, int term,
  * alpha[i*d + mu-1]; arrays must hold 3 terms (3*d alphas). */
 kx_status kx_scheme_coefficients(kx_scheme scheme, int ell, int d, int *nterms, double *eta,
                                  int *inner_ell, double *alpha);
+/* Host-only: Table 2 coefficients (complex), "+ in alpha_{1,mu}" branch; arrays hold 2 terms. */
+kx_status kx_scheme_coefficients_cplx(int ell, int d, int *nterms, double *eta_re, double *eta_im,
+                                      int *inner_ell, double *alpha_re, double *alpha_im);
 /* Library version string. */
 const char *kx_version(void);
 

@@ -82,4 +82,48 @@ int scheme_terms(int scheme, int ell, int d, double* eta, int* inner, double* al
   return 3;
 }
 
+// Table 2: complex two-term split, d >= 2, l = (1, 2), alpha independent of mu,
+// eta_2 carrying 2^{d-2}.  Branch: the paper's "+ in alpha_{1,mu}", i.e. the lower
+// sign of every -+/+- pair (reading R3): alpha_1 = 12/11 + 4 sqrt2/11 i for l = 1.
+int scheme_terms_cplx(int ell, int d, double* eta_re, double* eta_im, int* inner, double* alpha_re,
+                      double* alpha_im) {
+  if (d < 2 || (ell != 1 && ell != 2)) return 0;
+  const long double two = ldexpl(1.0L, d - 2);
+  long double e1r, e1i, a1r, a1i, e2r, e2i, a2r, a2i;
+  if (ell == 1) {
+    const long double r = sqrtl(2.0L);
+    e1r = 7.0L / 4.0L;
+    e1i = -3.0L * r / 2.0L;
+    a1r = 12.0L / 11.0L;
+    a1i = 4.0L * r / 11.0L;
+    e2r = two * -3.0L;
+    e2i = two * 6.0L * r;
+    a2r = 4.0L / 3.0L;
+    a2i = 2.0L * r / 3.0L;
+  } else {
+    const long double r = sqrtl(3.0L);
+    e1r = 2.0L / 3.0L;
+    e1i = -2.0L * r / 3.0L;
+    a1r = 3.0L / 4.0L;
+    a1i = r / 4.0L;
+    e2r = two * (-2.0L / 3.0L);
+    e2i = two * 8.0L * r / 3.0L;
+    a2r = 6.0L / 7.0L;
+    a2i = 3.0L * r / 7.0L;
+  }
+  eta_re[0] = (double)e1r;
+  eta_im[0] = (double)e1i;
+  eta_re[1] = (double)e2r;
+  eta_im[1] = (double)e2i;
+  inner[0] = 1;
+  inner[1] = 2;
+  for (int mu = 0; mu < d; ++mu) {
+    alpha_re[mu] = (double)a1r;
+    alpha_im[mu] = (double)a1i;
+    alpha_re[d + mu] = (double)a2r;
+    alpha_im[d + mu] = (double)a2i;
+  }
+  return 2;
+}
+
 }  // namespace kx

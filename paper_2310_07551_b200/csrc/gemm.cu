@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 namespace kx {
 namespace {
@@ -565,6 +566,11 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
       best = i;
     }
   }
+  static int forced = [] {
+    const char* e = getenv("KX_GEMM_CFG");   // tuning experiments only: 0, 1, 2
+    return e ? atoi(e) : -1;
+  }();
+  if (forced >= 0 && forced < 3) best = forced;
   if (g.arow) return vec ? launch_layout<true, 2>(g, nz, best, stream) : launch_layout<true, 1>(g, nz, best, stream);
   return vec ? launch_layout<false, 2>(g, nz, best, stream) : launch_layout<false, 1>(g, nz, best, stream);
 }

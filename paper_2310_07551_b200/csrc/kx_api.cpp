@@ -64,8 +64,9 @@ struct Stage {               // last-mode concatenated-K stage combination
 
 struct Chain {               // one phi-matrix family phi_{0,1,2}(sigma * A^c_mu)
   int c = 0, mu = 0;
-  double sigma = 0.0;
-  int q = 0;
+  double sigma = 0.0;          // real part of the scale
+  double sigma_im = 0.0;       // imaginary part (complex schemes: built on the real 2n x 2n
+  int q = 0;                   //  embedding [[Re, -Im], [Im, Re]] of sigma A)
 };
 
 }  // namespace
@@ -96,6 +97,7 @@ struct kx_ctx {
   bool bank_ready = false;
   long long bank_version = 0;
   int T = 0;                      // terms of the split scheme
+  bool cplx = false;              // complex split (Table 2): terms stored as (Re, Im) planes
   std::vector<Group> groups;
   std::map<std::pair<int, int>, PhiStack> phi;   // (ell, stage)
   Stage stages[3];
@@ -431,7 +433,45 @@ kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* c
   }
   double** cur = c->W1;
   double** nxt = c->W2;
-  for (int mu = d - 1; mu >= 2; --mu) {
+  for (int mu = d - 1; mu >= 2 && c->cplx; --mu) {
+    // complex terms (Re, Im planes): W' = P W  ->  Re = P_re W_re - P_im W_im,
+    // Im = P_re W_im + P_im W_re; four launches batched over terms, slabs and components
+    const long long nm = c->tn[mu - 1];
+    const long long R = prod_range(c, 1, mu - 1);
+    const long long Bt = prod_range(c, mu + 1, d);
+    const int pa[4] = {0, 1, 0, 1};   // plane of P
+    const int pw[4] = {0, 1, 1, 0};   // plane of W read
+    const int po[4] = {0, 0, 1, 1};   // plane of W' written
+    const double al[4] = {1.0, -1.0, 1.0, 1.0};
+    for (int k = 0; k < 4; ++k) {
+      GemmArgs g;
+      g.arow = false;
+      g.M = (int)nm;
+      g.N = (int)R;
+      g.kseg = (int)nm;
+      g.lda = nm;
+      g.ldb = R;
+      g.ldc = R;
+      g.ldd = R;
+      g.ns = ns;
+      g.nt = nt / 2;
+      g.nb = (int)Bt;
+      g.sA_t = 2 * nm * nm;
+      g.sB_t = g.sC_t = g.sD_t = 2 * N;
+      g.sB_b = g.sC_b = g.sD_b = nm * R;
+      g.alpha = al[k];
+      g.beta = (k == 1 || k == 3) ? 1.0 : 0.0;
+      for (int s = 0; s < ns; ++s) {
+        g.A[s] = G.mid[s][mu - 1] + (t0 + pa[k]) * nm * nm;
+        g.B[s] = cur[s] + (long long)(slot + pw[k]) * N;
+        g.C[s] = nxt[s] + (long long)(slot + po[k]) * N;
+        g.D[s] = g.beta != 0.0 ? g.C[s] : nullptr;
+      }
+      KX_TRY(run_gemm(c, g));
+    }
+    std::swap(cur, nxt);
+  }
+  for (int mu = d - 1; mu >= 2 && !c->cplx; --mu) {
     const long long nm = c->tn[mu - 1];
     const long long R = prod_range(c, 1, mu - 1);
     const long long Bt = prod_range(c, mu + 1, d);
@@ -531,7 +571,7 @@ kx_status enqueue_step_etd3(kx_ctx* c, double* const* U) {
   KX_TRY(group_modes(c, c->groups[2], 0, c->groups[2].nterms, c->D, c->groups[2].slot0, &ws));
   KX_TRY(last_mode_concat(c, ws, nullptr, c->stages[2].nseg, c->stages[2].slot, c->stages[2].B,
                           U, 1.0, 1.0, U));
-  c->cnt.tucker_ops += (long long)ns * (c->groups[0].nterms + 2 * c->T);
+  c->cnt.tucker_ops += (long long)ns * 5 * c->T;   // 3T on F, T on D2, T on D3
   return KX_OK;
 }
 
@@ -551,7 +591,7 @@ kx_status enqueue_step_etd2(kx_ctx* c, double* const* U) {
 }
 
 kx_status enqueue_step(kx_ctx* c, double* const* U) {
-  if (c->scheme == KX_ETD3RKDS_REAL) return enqueue_step_etd3(c, U);
+  if (c->scheme == KX_ETD3RKDS_REAL || c->scheme == KX_ETD3RKDS_CPLX) return enqueue_step_etd3(c, U);
   return enqueue_step_etd2(c, U);
 }
 
@@ -610,10 +650,11 @@ struct ChainOut {
   double* p[3][2] = {};
 };
 
-kx_status build_chains(kx_ctx* c, long long n, std::vector<Chain>& ch, bool thirds,
+kx_status build_chains(kx_ctx* c, long long n_a, bool emb, std::vector<Chain>& ch, bool thirds,
                        std::vector<ChainOut>& out, std::vector<double*>& scratch) {
   const int C = (int)ch.size();
   if (C == 0) return KX_OK;
+  const long long n = emb ? 2 * n_a : n_a;   // matrix size of the chain arithmetic
   const long long n2 = n * n;
   // sort by q descending (active chains in a doubling round form a prefix)
   std::vector<int> order(C);
@@ -637,9 +678,19 @@ kx_status build_chains(kx_ctx* c, long long n, std::vector<Chain>& ch, bool thir
   // X_k = sigma_k 2^{-q_k} A  (position k in sorted order)
   for (int k = 0; k < C; ++k) {
     const Chain& h = ch[order[k]];
-    const double scale = std::ldexp(h.sigma, -h.q);
+    const double sre = std::ldexp(h.sigma, -h.q), sim = std::ldexp(h.sigma_im, -h.q);
     const double* Ad = c->A_dev[h.c][h.mu - 1];
-    KX_TRY(run_other(c, [&] { return kx::launch_scale(X + k * n2, Ad, scale, n2, c->cur); }));
+    double* Xk = X + k * n2;
+    if (!emb) {
+      KX_TRY(run_other(c, [&] { return kx::launch_scale(Xk, Ad, sre, n2, c->cur); }));
+    } else {
+      // row-major [[sre A^T, -sim A^T], [sim A^T, sre A^T]]  (A's column-major buffer = A^T)
+      const long long m = n_a;
+      KX_TRY(run_other(c, [&] { return kx::launch_copy2d(Xk, n, 0, Ad, m, 0, m, m, 1, sre, c->cur); }));
+      KX_TRY(run_other(c, [&] { return kx::launch_copy2d(Xk + m, n, 0, Ad, m, 0, m, m, 1, -sim, c->cur); }));
+      KX_TRY(run_other(c, [&] { return kx::launch_copy2d(Xk + m * n, n, 0, Ad, m, 0, m, m, 1, sim, c->cur); }));
+      KX_TRY(run_other(c, [&] { return kx::launch_copy2d(Xk + m * n + m, n, 0, Ad, m, 0, m, m, 1, sre, c->cur); }));
+    }
   }
   // Horner for phi_2: H = I/(K+2)!; H = X H + I/(k+2)!, k = K-1..0
   double fact[TAYLOR_K + 3];
@@ -701,30 +752,33 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
   drop_bank(c);
   c->scheme = scheme;
   c->tau = tau;
-  const bool etd3 = scheme == KX_ETD3RKDS_REAL;
-  // --- coefficients
-  double eta[2][3], alpha[2][3 * KX_MAXD];
+  const bool cplx = scheme == KX_ETD3RKDS_CPLX;
+  const bool etd3 = scheme == KX_ETD3RKDS_REAL || cplx;
+  const int pl = cplx ? 2 : 1;   // real planes per term (Re, Im for the complex split)
+  c->cplx = cplx;
+  // --- coefficients (imaginary parts zero for the real schemes)
+  double eta[2][3] = {}, eta_im[2][3] = {}, alpha[2][3 * KX_MAXD] = {}, alpha_im[2][3 * KX_MAXD] = {};
   int inner[2][3];
   int T = 0;
   for (int ell = 1; ell <= 2; ++ell) {
-    int t = kx::scheme_terms(scheme, ell, d, eta[ell - 1], inner[ell - 1], alpha[ell - 1]);
+    const int t = cplx ? kx::scheme_terms_cplx(ell, d, eta[ell - 1], eta_im[ell - 1], inner[ell - 1],
+                                               alpha[ell - 1], alpha_im[ell - 1])
+                       : kx::scheme_terms(scheme, ell, d, eta[ell - 1], inner[ell - 1], alpha[ell - 1]);
     if (t == 0) return fail(c, KX_ERR_UNSUPPORTED, "scheme not available for this d");
     T = t;
   }
   c->T = T;
-  // --- groups, levels, chains.  Chain key: (c, mu, ell-target, term) with
-  // sigma = (tau/3) alpha (ETD3, levels 1/3 -> 2/3 -> 1) or tau (ETD2, level 1).
-  struct Need { int group, term, c, mu, ellt, tt, level; };
+  // --- groups (input tensors) of terms; every term occupies `pl` real planes / slots
   std::vector<Group> groups;
   if (etd3) {
     groups.resize(3);
-    groups[0].nterms = 3 * T;  // F: (stage 1/3, l=1) (2/3, l=1) (1, l=1)
-    groups[1].nterms = T;      // D2: (2/3, l=2)
-    groups[2].nterms = T;      // D3: (1, l=2)
+    groups[0].nterms = 3 * T * pl;  // F: (stage 1/3, l=1) (2/3, l=1) (1, l=1)
+    groups[1].nterms = T * pl;      // D2: (2/3, l=2)
+    groups[2].nterms = T * pl;      // D3: (1, l=2)
     groups[0].slot0 = 0;
-    groups[1].slot0 = 3 * T;
-    groups[2].slot0 = 3 * T;
-    c->nslots = 4 * T;
+    groups[1].slot0 = 3 * T * pl;
+    groups[2].slot0 = 3 * T * pl;
+    c->nslots = 4 * T * pl;
   } else {
     groups.resize(2);
     groups[0].nterms = 1;
@@ -733,11 +787,11 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
     groups[1].slot0 = 1;
     c->nslots = 2;
   }
-  // unique chains (dedupe identical (A, sigma))
-  std::vector<std::vector<Chain>> chains_by_n;   // grouped by extent
-  std::vector<long long> ext;                    // extent of each bucket
+  // --- unique chains (dedupe identical (A, sigma)), bucketed by matrix extent
+  std::vector<std::vector<Chain>> chains_by_n;
+  std::vector<long long> ext;
   struct ChainRef { int bucket, idx; };
-  auto find_or_add = [&](int comp, int mu, double sigma) -> ChainRef {
+  auto find_or_add = [&](int comp, int mu, double sre, double sim) -> ChainRef {
     const long long n = c->n[mu - 1];
     int bkt = -1;
     for (size_t i = 0; i < ext.size(); ++i)
@@ -749,31 +803,33 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
     }
     auto& v = chains_by_n[bkt];
     for (size_t i = 0; i < v.size(); ++i) {
-      if (v[i].sigma == sigma && c->A_host[v[i].c][v[i].mu - 1] == c->A_host[comp][mu - 1])
+      if (v[i].sigma == sre && v[i].sigma_im == sim &&
+          c->A_host[v[i].c][v[i].mu - 1] == c->A_host[comp][mu - 1])
         return {bkt, (int)i};
     }
     Chain h;
     h.c = comp;
     h.mu = mu;
-    h.sigma = sigma;
-    const double nrm = std::fabs(sigma) * norm_bound(c->A_host[comp][mu - 1], n);
+    h.sigma = sre;
+    h.sigma_im = sim;
+    const double nrm = (std::fabs(sre) + std::fabs(sim)) * norm_bound(c->A_host[comp][mu - 1], n);
     h.q = nrm > THETA ? (int)std::ceil(std::log2(nrm / THETA)) : 0;
     v.push_back(h);
     return {bkt, (int)v.size() - 1};
   };
-  // refs[g][c][t][mu-1] -> (chain, level, l)
+  // refs[g][comp][term][mu-1] -> (chain, level, l); term indexes complex terms
   struct Ref { ChainRef ch; int level; int l; };
   std::vector<std::vector<std::vector<std::vector<Ref>>>> refs(groups.size());
-  for (size_t gi = 0; gi < groups.size(); ++gi) {
-    refs[gi].assign(nc, std::vector<std::vector<Ref>>(groups[gi].nterms, std::vector<Ref>(d)));
-  }
+  for (size_t gi = 0; gi < groups.size(); ++gi)
+    refs[gi].assign(nc, std::vector<std::vector<Ref>>(groups[gi].nterms / pl, std::vector<Ref>(d)));
   for (int comp = 0; comp < nc; ++comp) {
     for (int mu = 1; mu <= d; ++mu) {
       if (etd3) {
         for (int ellt = 1; ellt <= 2; ++ellt) {
           for (int i = 0; i < T; ++i) {
-            const double sigma = tau / 3.0 * alpha[ellt - 1][i * d + mu - 1];
-            ChainRef r = find_or_add(comp, mu, sigma);
+            const double sre = tau / 3.0 * alpha[ellt - 1][i * d + mu - 1];
+            const double sim = tau / 3.0 * alpha_im[ellt - 1][i * d + mu - 1];
+            ChainRef r = find_or_add(comp, mu, sre, sim);
             const int l = inner[ellt - 1][i];
             if (ellt == 1) {
               for (int lev = 0; lev < 3; ++lev) refs[0][comp][lev * T + i][mu - 1] = {r, lev, l};
@@ -784,7 +840,7 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
           }
         }
       } else {
-        ChainRef r = find_or_add(comp, mu, tau);
+        ChainRef r = find_or_add(comp, mu, tau, 0.0);
         refs[0][comp][0][mu - 1] = {r, 2, 1};
         refs[1][comp][0][mu - 1] = {r, 2, 2};
       }
@@ -797,51 +853,75 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
   } scratch_guard;
   std::vector<double*>& scratch = scratch_guard.v;
   std::vector<std::vector<ChainOut>> outs(chains_by_n.size());
-  for (size_t b = 0; b < chains_by_n.size(); ++b) {
-    KX_TRY(build_chains(c, ext[b], chains_by_n[b], etd3, outs[b], scratch));
-  }
-  auto chain_ptr = [&](const Ref& r) { return outs[r.ch.bucket][r.ch.idx].p[r.level][r.l - 1]; };
-  // --- lay out the bank
+  for (size_t b = 0; b < chains_by_n.size(); ++b)
+    KX_TRY(build_chains(c, ext[b], cplx, chains_by_n[b], etd3, outs[b], scratch));
+  // plane `part` (0 = Re, 1 = Im) of a referenced phi-matrix, column-major with leading dim ld
+  auto plane_src = [&](const Ref& r, int part, long long n, long long* ld) -> const double* {
+    const double* p = outs[r.ch.bucket][r.ch.idx].p[r.level][r.l - 1];
+    if (!cplx) {
+      *ld = n;
+      return p;
+    }
+    *ld = 2 * n;
+    return part == 0 ? p : p + n * 2 * n;
+  };
+  // --- lay out the bank (planes of term t: t*pl + part)
   const long long n1 = c->n[0], nd = c->n[d - 1];
   auto bal = [&](double** p, size_t cnt) { return dalloc(c, p, cnt, c->bank_allocs); };
   for (size_t gi = 0; gi < groups.size(); ++gi) {
     Group& G = groups[gi];
-    const int TG = G.nterms;
+    const int TG = G.nterms;   // planes
     for (int comp = 0; comp < nc; ++comp) {
       KX_TRY(bal(&G.last[comp], (size_t)TG * n1 * n1));
-      for (int t = 0; t < TG; ++t)
-        KX_CUDA(c, cudaMemcpyAsync(G.last[comp] + t * n1 * n1, chain_ptr(refs[gi][comp][t][0]),
-                                   n1 * n1 * 8, cudaMemcpyDeviceToDevice, c->cur));
-      if (d >= 2) {
-        KX_TRY(bal(&G.first[comp], (size_t)TG * nd * nd));
-        for (int t = 0; t < TG; ++t)
-          KX_CUDA(c, cudaMemcpy2DAsync(G.first[comp] + t * nd, TG * nd * 8,
-                                       chain_ptr(refs[gi][comp][t][d - 1]), nd * 8, nd * 8, nd,
+      if (d >= 2) KX_TRY(bal(&G.first[comp], (size_t)TG * nd * nd));
+      for (int mu = 2; mu < d; ++mu) KX_TRY(bal(&G.mid[comp][mu - 1], (size_t)TG * c->n[mu - 1] * c->n[mu - 1]));
+      for (int t = 0; t < TG / pl; ++t) {
+        for (int part = 0; part < pl; ++part) {
+          const int plane = t * pl + part;
+          long long ld;
+          const double* src = plane_src(refs[gi][comp][t][0], part, n1, &ld);
+          KX_CUDA(c, cudaMemcpy2DAsync(G.last[comp] + plane * n1 * n1, n1 * 8, src, ld * 8, n1 * 8, n1,
                                        cudaMemcpyDeviceToDevice, c->cur));
-      }
-      for (int mu = 2; mu < d; ++mu) {
-        const long long nm = c->n[mu - 1];
-        KX_TRY(bal(&G.mid[comp][mu - 1], (size_t)TG * nm * nm));
-        for (int t = 0; t < TG; ++t)
-          KX_CUDA(c, cudaMemcpyAsync(G.mid[comp][mu - 1] + t * nm * nm,
-                                     chain_ptr(refs[gi][comp][t][mu - 1]), nm * nm * 8,
-                                     cudaMemcpyDeviceToDevice, c->cur));
+          if (d >= 2) {
+            src = plane_src(refs[gi][comp][t][d - 1], part, nd, &ld);
+            KX_CUDA(c, cudaMemcpy2DAsync(G.first[comp] + plane * nd, (size_t)TG * nd * 8, src, ld * 8,
+                                         nd * 8, nd, cudaMemcpyDeviceToDevice, c->cur));
+          }
+          for (int mu = 2; mu < d; ++mu) {
+            const long long nm = c->n[mu - 1];
+            src = plane_src(refs[gi][comp][t][mu - 1], part, nm, &ld);
+            KX_CUDA(c, cudaMemcpy2DAsync(G.mid[comp][mu - 1] + plane * nm * nm, nm * 8, src, ld * 8,
+                                         nm * 8, nm, cudaMemcpyDeviceToDevice, c->cur));
+          }
+        }
       }
     }
   }
-  // phi stacks for kx_phi_apply: block t = eta_t P_t{1}
+  // Last-mode blocks: the real part of kappa * eta_t * (W_t x_1 P_t{1}) for a complex term is
+  //   W_re x_1 Re(kappa eta P) + W_im x_1 (-Im(kappa eta P)),
+  // so a term contributes the blocks [Re(kappa eta P); -Im(kappa eta P)] over its two slots.
+  auto put_blocks = [&](double* dst, int gi, int comp, int t, double kre, double kim) -> kx_status {
+    const long long m2 = n1 * n1;
+    const Group& G = groups[gi];
+    if (!cplx) {
+      const double* src = G.last[comp] + t * m2;
+      return run_other(c, [&] { return kx::launch_scale(dst, src, kre, m2, c->cur); });
+    }
+    const double* Pre = G.last[comp] + (2 * t) * m2;
+    const double* Pim = G.last[comp] + (2 * t + 1) * m2;
+    KX_TRY(run_other(c, [&] { return kx::launch_axpby(dst, kre, Pre, -kim, Pim, m2, c->cur); }));
+    return run_other(c, [&] { return kx::launch_axpby(dst + m2, -kre, Pim, -kim, Pre, m2, c->cur); });
+  };
+  // phi stacks for kx_phi_apply: (Re part of) sum_t eta_t T(X, P_t)
   auto make_stack = [&](PhiStack& ps, int gi, int t0, int ell) -> kx_status {
     ps.group = gi;
-    ps.t0 = t0;
-    ps.nterms = T;
+    ps.t0 = t0 * pl;
+    ps.nterms = T * pl;
     for (int comp = 0; comp < nc; ++comp) {
-      KX_TRY(bal(&ps.B[comp], (size_t)T * n1 * n1));
-      for (int t = 0; t < T; ++t) {
-        const double* src = groups[gi].last[comp] + (t0 + t) * n1 * n1;
-        const double e = eta[ell - 1][t];
-        double* dst = ps.B[comp] + t * n1 * n1;
-        KX_TRY(run_other(c, [&] { return kx::launch_scale(dst, src, e, n1 * n1, c->cur); }));
-      }
+      KX_TRY(bal(&ps.B[comp], (size_t)T * pl * n1 * n1));
+      for (int t = 0; t < T; ++t)
+        KX_TRY(put_blocks(ps.B[comp] + (size_t)t * pl * n1 * n1, gi, comp, t0 + t, eta[ell - 1][t],
+                          eta_im[ell - 1][t]));
     }
     return KX_OK;
   };
@@ -853,36 +933,34 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
     KX_TRY(make_stack(c->phi[{1, 2}], 0, 0, 1));
     KX_TRY(make_stack(c->phi[{2, 2}], 1, 0, 2));
   }
-  // stage stacks (eq:exprk3 P:586-594 scalars folded in)
-  struct Seg { int gi, t, slot; double scale; };
+  // stage stacks (eq:exprk3 P:586-594 scalars folded in): (group, term, slot of plane 0, kappa*eta)
+  struct Seg { int gi, t, slot; double kre, kim; };
   auto make_stage = [&](Stage& S, const std::vector<Seg>& segs) -> kx_status {
-    S.nseg = (int)segs.size();
-    for (int k = 0; k < S.nseg; ++k) S.slot[k] = segs[k].slot;
+    S.nseg = (int)segs.size() * pl;
+    for (size_t k = 0; k < segs.size(); ++k)
+      for (int part = 0; part < pl; ++part) S.slot[k * pl + part] = segs[k].slot + part;
     for (int comp = 0; comp < nc; ++comp) {
       KX_TRY(bal(&S.B[comp], (size_t)S.nseg * n1 * n1));
-      for (int k = 0; k < S.nseg; ++k) {
-        const double* src = groups[segs[k].gi].last[comp] + segs[k].t * n1 * n1;
-        double* dst = S.B[comp] + k * n1 * n1;
-        const double sc = segs[k].scale;
-        KX_TRY(run_other(c, [&] { return kx::launch_scale(dst, src, sc, n1 * n1, c->cur); }));
-      }
+      for (size_t k = 0; k < segs.size(); ++k)
+        KX_TRY(put_blocks(S.B[comp] + k * pl * n1 * n1, segs[k].gi, comp, segs[k].t, segs[k].kre, segs[k].kim));
     }
     return KX_OK;
   };
   if (etd3) {
     std::vector<Seg> s0, s1, s2;
-    for (int i = 0; i < T; ++i) s0.push_back({0, i, i, tau / 3.0 * eta[0][i]});
-    for (int i = 0; i < T; ++i) s1.push_back({0, T + i, T + i, 2.0 * tau / 3.0 * eta[0][i]});
-    for (int i = 0; i < T; ++i) s1.push_back({1, i, 3 * T + i, 4.0 * tau / 3.0 * eta[1][i]});
-    for (int i = 0; i < T; ++i) s2.push_back({0, 2 * T + i, 2 * T + i, tau * eta[0][i]});
-    for (int i = 0; i < T; ++i) s2.push_back({2, i, 3 * T + i, 1.5 * tau * eta[1][i]});
+    const double k0 = tau / 3.0, k1 = 2.0 * tau / 3.0, k1d = 4.0 * tau / 3.0, k2 = tau, k2d = 1.5 * tau;
+    for (int i = 0; i < T; ++i) s0.push_back({0, i, i * pl, k0 * eta[0][i], k0 * eta_im[0][i]});
+    for (int i = 0; i < T; ++i) s1.push_back({0, T + i, (T + i) * pl, k1 * eta[0][i], k1 * eta_im[0][i]});
+    for (int i = 0; i < T; ++i) s1.push_back({1, i, (3 * T + i) * pl, k1d * eta[1][i], k1d * eta_im[1][i]});
+    for (int i = 0; i < T; ++i) s2.push_back({0, 2 * T + i, (2 * T + i) * pl, k2 * eta[0][i], k2 * eta_im[0][i]});
+    for (int i = 0; i < T; ++i) s2.push_back({2, i, (3 * T + i) * pl, k2d * eta[1][i], k2d * eta_im[1][i]});
     KX_TRY(make_stage(c->stages[0], s0));
     KX_TRY(make_stage(c->stages[1], s1));
     KX_TRY(make_stage(c->stages[2], s2));
     c->nstages = 3;
   } else {
-    KX_TRY(make_stage(c->stages[0], {{0, 0, 0, tau * eta[0][0]}}));
-    KX_TRY(make_stage(c->stages[1], {{1, 0, 1, tau * eta[1][0]}}));
+    KX_TRY(make_stage(c->stages[0], {{0, 0, 0, tau * eta[0][0], 0.0}}));
+    KX_TRY(make_stage(c->stages[1], {{1, 0, 1, tau * eta[1][0], 0.0}}));
     c->nstages = 2;
   }
   c->groups = groups;
@@ -1208,11 +1286,11 @@ kx_status dist_d_source(kx_ctx* c, Exchange& x) {
   return KX_OK;
 }
 
-int dist_phases(const kx_ctx* c) { return c->scheme == KX_ETD3RKDS_REAL ? 7 : 5; }
+int dist_phases(const kx_ctx* c) { return c->scheme == KX_ETD2RKDS ? 5 : 7; }
 
 kx_status dist_phase(kx_ctx* c, double* const* U, int ph, Exchange& x) {
   x = Exchange{};
-  const bool e3 = c->scheme == KX_ETD3RKDS_REAL;
+  const bool e3 = c->scheme != KX_ETD2RKDS;
   const double* Uc[MAXS];
   const double* Usc[MAXS];
   for (int s = 0; s < c->ncomp; ++s) {
@@ -1239,7 +1317,7 @@ kx_status dist_phase(kx_ctx* c, double* const* U, int ph, Exchange& x) {
     case 5: return dist_group(c, 2, c->D_B, x);
     case 6:
       KX_TRY(dist_stage(c, c->stages[2], U, Uc));
-      c->cnt.tucker_ops += (long long)c->ncomp * (c->groups[0].nterms + 2 * c->T);
+      c->cnt.tucker_ops += (long long)c->ncomp * 5 * c->T;
       return KX_OK;
   }
   return fail(c, KX_ERR_INVALID, "bad phase");
@@ -1478,10 +1556,10 @@ kx_status kx_set_model(kx_ctx* c, kx_model model, const double* params, int npar
 kx_status kx_set_tau(kx_ctx* c, double tau, kx_scheme scheme) {
   KX_TRY(need_grid(c));
   if (!(tau > 0.0) || !std::isfinite(tau)) return fail(c, KX_ERR_INVALID, "tau must be > 0");
-  if (scheme != KX_ETD2RKDS && scheme != KX_ETD3RKDS_REAL)
+  if (scheme != KX_ETD2RKDS && scheme != KX_ETD3RKDS_REAL && scheme != KX_ETD3RKDS_CPLX)
     return fail(c, KX_ERR_INVALID, "unknown scheme");
-  if (scheme == KX_ETD3RKDS_REAL && c->d < 2)
-    return fail(c, KX_ERR_UNSUPPORTED, "exprk3ds_real needs d >= 2 (Tables 1 and 3)");
+  if (scheme != KX_ETD2RKDS && c->d < 2)
+    return fail(c, KX_ERR_UNSUPPORTED, "exprk3ds needs d >= 2 (Tables 1-3)");
   for (int comp = 0; comp < c->ncomp; ++comp)
     for (int mu = 1; mu <= c->d; ++mu)
       if (c->A_host[comp][mu - 1].empty())
@@ -1837,6 +1915,15 @@ kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const
   }
   for (int r = 0; r < nranks; ++r) ctxs[r]->cnt.steps += 1;
   return KX_OK;
+}
+
+kx_status kx_scheme_coefficients_cplx(int ell, int d, int* nterms, double* eta_re, double* eta_im,
+                                      int* inner_ell, double* alpha_re, double* alpha_im) {
+  if (!nterms || !eta_re || !eta_im || !inner_ell || !alpha_re || !alpha_im) return KX_ERR_INVALID;
+  if (d < 1 || d > KX_MAXD) return KX_ERR_INVALID;
+  const int t = kx::scheme_terms_cplx(ell, d, eta_re, eta_im, inner_ell, alpha_re, alpha_im);
+  *nterms = t;
+  return t ? KX_OK : KX_ERR_UNSUPPORTED;
 }
 
 kx_status kx_scheme_coefficients(kx_scheme scheme, int ell, int d, int* nterms, double* eta,

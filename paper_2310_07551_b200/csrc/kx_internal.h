@@ -82,6 +82,9 @@ cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream);
 
 // Y = alpha * X (elementwise, n doubles); used for bank assembly.
 cudaError_t launch_scale(double* Y, const double* X, double alpha, long long n, cudaStream_t s);
+// Y = a X1 + b X2 (elementwise, n doubles); complex bank blocks.
+cudaError_t launch_axpby(double* Y, double a, const double* X1, double b, const double* X2, long long n,
+                         cudaStream_t s);
 // Strided matrix copy with scale: Y[r*ldy + c] = alpha * X[r*ldx + c], rows x cols, batched
 // over nbatch with strides sy / sx.
 cudaError_t launch_copy2d(double* Y, long long ldy, long long sy, const double* X, long long ldx,
@@ -94,5 +97,7 @@ cudaError_t launch_check_finite(const double* X, long long n, int* flag, cudaStr
 
 // Split coefficient tables (host).  Returns number of terms (0 if unsupported).
 int scheme_terms(int scheme, int ell, int d, double* eta, int* inner, double* alpha);
+int scheme_terms_cplx(int ell, int d, double* eta_re, double* eta_im, int* inner, double* alpha_re,
+                      double* alpha_im);
 
 }  // namespace kx

@@ -92,6 +92,13 @@ __global__ void scale_kernel(double* __restrict__ y, const double* __restrict__ 
     y[i] = alpha * x[i];
 }
 
+__global__ void axpby_kernel(double* __restrict__ y, double a, const double* __restrict__ x1, double b,
+                             const double* __restrict__ x2, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x1[i] + b * x2[i];
+}
+
 __global__ void copy2d_kernel(double* __restrict__ y, long long ldy, long long sy,
                               const double* __restrict__ x, long long ldx, long long sx,
                               long long rows, long long cols, double alpha) {
@@ -220,6 +227,13 @@ cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream) {
 cudaError_t launch_scale(double* Y, const double* X, double alpha, long long n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(Y, X, alpha, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpby(double* Y, double a, const double* X1, double b, const double* X2, long long n,
+                         cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  axpby_kernel<<<grid_for(n, 256), 256, 0, s>>>(Y, a, X1, b, X2, n);
   return cudaGetLastError();
 }
 

@@ -19,11 +19,11 @@ LIB_PATH = os.path.join(_HERE, "libkx.so")
 
 KX_OK, KX_ERR_INVALID, KX_ERR_NUMERIC, KX_ERR_IO = 0, 2, 3, 4
 KX_ERR_CUDA, KX_ERR_NCCL, KX_ERR_UNSUPPORTED, KX_ERR_NOMEM = 5, 6, 7, 8
-KX_ETD2RKDS, KX_ETD3RKDS_REAL = 1, 2
+KX_ETD2RKDS, KX_ETD3RKDS_REAL, KX_ETD3RKDS_CPLX = 1, 2, 3
 KX_MODEL_NONE, KX_MODEL_SCHNAKENBERG, KX_MODEL_FHN = 0, 1, 2
 
 SCHEMES = {"etd2rkds": KX_ETD2RKDS, "etd3rkds": KX_ETD3RKDS_REAL,
-           "exprk3ds_real": KX_ETD3RKDS_REAL}
+           "exprk3ds_real": KX_ETD3RKDS_REAL, "exprk3ds_cplx": KX_ETD3RKDS_CPLX}
 MODELS = {"none": KX_MODEL_NONE, "schnakenberg": KX_MODEL_SCHNAKENBERG, "fhn": KX_MODEL_FHN}
 
 
@@ -74,6 +74,7 @@ _SIGS = {
     "kx_get_profile": (_i, [_vp, _dp, _dp, C.POINTER(_ll), C.POINTER(_ll), _dp]),
     "kx_get_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
     "kx_scheme_coefficients": (_i, [_i, _i, _i, C.POINTER(_i), _dp, C.POINTER(_i), _dp]),
+    "kx_scheme_coefficients_cplx": (_i, [_i, _i, C.POINTER(_i), _dp, _dp, C.POINTER(_i), _dp, _dp]),
     "kx_version": (C.c_char_p, []),
 }
 EXPORTED = tuple(_SIGS)
@@ -119,6 +120,20 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def scheme_coefficients_cplx(ell: int, d: int):
+    """Host-only: Table 2 (etas, inner ells, alphas[i][mu]) as complex numbers."""
+    nt = C.c_int(0)
+    er, ei = (C.c_double * 3)(), (C.c_double * 3)()
+    inner = (C.c_int * 3)()
+    ar, ai = (C.c_double * (3 * d))(), (C.c_double * (3 * d))()
+    st = kx_scheme_coefficients_cplx(ell, d, C.byref(nt), er, ei, inner, ar, ai)
+    if st != KX_OK:
+        raise KxError(st, "scheme not available")
+    n = nt.value
+    return ([complex(er[i], ei[i]) for i in range(n)], list(inner[:n]),
+            [[complex(ar[i * d + m], ai[i * d + m]) for m in range(d)] for i in range(n)])
+
+
 class Context:
     """Owns one kx_ctx.  Methods mirror the C ABI one to one.
 
@@ -157,7 +172,11 @@ class Context:
             kx_destroy(self.h)
             self.h = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # interpreter teardown: the ctypes globals may already be gone
+            pass
 
     # --- setup
     def set_grid(self, n: list[int], ncomp: int = 2):

@@ -64,3 +64,12 @@ def test_create_without_gpu_fails_cleanly(kx):
     assert st == kx.KX_ERR_CUDA
     assert kx.kx_create_error()
     assert kx.kx_set_grid(None, 2, None, 2) == kx.KX_ERR_INVALID
+
+
+@pytest.mark.parametrize("ell", [1, 2])
+@pytest.mark.parametrize("d", [2, 3, 4])
+def test_complex_coefficients_match_oracle(kx, ell, d):
+    from oracle import coeffs
+    eta, inner, alpha = kx.scheme_coefficients_cplx(ell, d)
+    ref = coeffs.table2(ell, d)
+    assert eta == ref.etas and inner == ref.inner and alpha == ref.alphas

@@ -442,3 +442,66 @@ def test_no_out_of_bounds_writes(ctx, n, G):
     for b in [big] + bigU:
         v = b[:G].cpu().numpy().tolist() + b[G + N:].cpu().numpy().tolist()
         assert len(set(v)) == 1, "guard band overwritten"
+
+
+@pytest.mark.parametrize("case", [("schnakenberg", 2, 48, 1e-4), ("fhn", 3, 20, 0.015), ("fhn", 3, 17, 0.01)])
+def test_complex_bank_and_phi_apply(ctx, case):
+    """exprk3ds_cplx (Table 2): complex phi-matrices via the real 2n x 2n embedding on the GPU
+    against the oracle's complex Taylor/doubling phi, and the real part of the split action."""
+    model, d, n, tau = case
+    prob = inputs.make_problem(model, d, n)
+    setup_problem(ctx, prob, "exprk3ds_cplx", tau)
+    s = {1: coeffs.table2(1, d), 2: coeffs.table2(2, d)}
+    cs = {0: 1 / 3, 1: 2 / 3, 2: 1.0}
+    x = tensor(prob.n, 31)
+    for c in range(2):
+        for (ell, stage) in [(1, 0), (1, 1), (1, 2), (2, 1), (2, 2)]:
+            for i in range(2):
+                for mu in range(1, d + 1):
+                    X = cs[stage] * tau * s[ell].alphas[i][mu - 1] * prob.A[c][mu - 1]
+                    ref = phi_matrices(X, 2)[s[ell].inner[i]]
+                    re = ctx.phi_matrix(c, ell, stage, 2 * i, mu)
+                    im = ctx.phi_matrix(c, ell, stage, 2 * i + 1, mu)
+                    assert relerr(re + 1j * im, ref) <= 1e-11
+            P = split_phi_matrices(s[ell], cs[stage] * tau, prob.A[c])
+            ref = np.real(vec(split_apply(s[ell].etas, P, unvec(x, prob.n))))
+            Y = dev(np.zeros(x.size))
+            ctx.phi_apply(c, ell, stage, dev(x), Y)
+            assert relerr(Y.cpu().numpy(), ref) <= 1e-11
+
+
+@pytest.mark.parametrize("case", [("schnakenberg", 2, 64, 2.0, 6000, 10), ("fhn", 3, 24, 150.0, 10000, 10),
+                                  ("schnakenberg", 2, 50, 0.25, 1000, 5)])
+def test_complex_step_parity(ctx, case):
+    model, d, n, T, m, steps = case
+    prob = inputs.make_problem(model, d, n, seed=4)
+    tau = T / m
+    setup_problem(ctx, prob, "exprk3ds_cplx", tau)
+    out = run_gpu(ctx, prob, "exprk3ds_cplx", tau, steps)
+    ref, _ = integrate(prob, "exprk3ds_cplx", T=T, m=m, steps=steps)
+    err = max(relerr(out[c], ref[c]) for c in range(2))
+    assert err <= 1e-10, err
+    cnt = ctx.counters()
+    assert cnt["tucker_ops"] == steps * 2 * 10 and cnt["kronsum_actions"] == steps * 2
+
+
+def test_complex_sharded_loopback(kx):
+    prob = inputs.make_problem("fhn", 3, [16, 12, 16], seed=6)
+    tau, P = 0.015, 2
+    one = kx.Context(0)
+    setup_problem(one, prob, "exprk3ds_cplx", tau)
+    grp = kx.Group(P)
+    for c in grp.ctx:
+        setup_problem(c, prob, "exprk3ds_cplx", tau)
+    U1 = [dev(u) for u in prob.U0]
+    Ug = [[dev(slab(prob.U0[s], prob.n, r, P)) for s in range(2)] for r in range(P)]
+    for _ in range(2):
+        one.step(U1)
+        grp.step(Ug)
+    one.sync()
+    grp.ctx[0].sync()
+    for s in range(2):
+        parts = [unvec(Ug[r][s].cpu().numpy(), prob.n[:-1] + [prob.n[-1] // P]) for r in range(P)]
+        assert relerr(vec(np.concatenate(parts, axis=-1)), U1[s].cpu().numpy()) <= 1e-13
+    grp.close()
+    one.close()
