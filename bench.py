@@ -136,13 +136,18 @@ def oracle_sample(cfg_name, seconds):
     rs = np.random.default_rng(0)
     # phi-bank formation (setup, ~7 TFLOP for C2 in the oracle) is replaced by random dense
     # matrices of the same shapes: the per-step cost does not depend on their values.
-    if cfg["scheme"] == "etd3rkds":
-        s1, s2 = coeffs.etd3_scheme(1, d), coeffs.etd3_scheme(2, d)
+    if cfg["scheme"] in ("etd3rkds", "exprk3ds_cplx"):
+        variant = "cplx" if cfg["scheme"] == "exprk3ds_cplx" else "real"
+        s1, s2 = coeffs.etd3_scheme(1, d, variant), coeffs.etd3_scheme(2, d, variant)
         bank = Exprk3Bank(tau, s1, s2)
+
+        def rnd(n):
+            m = rs.uniform(0, 1.0 / n, (n, n))
+            return m + 1j * rs.uniform(0, 1.0 / n, (n, n)) if variant == "cplx" else m
         for c in range(2):
             Pc = {}
             for key in [("2", 1), ("3", 1), ("3", 2), ("f", 1), ("f", 2)]:
-                Pc[key] = [[rs.uniform(0, 1.0 / n, (n, n)) for n in prob.n] for _ in range(s1.nterms)]
+                Pc[key] = [[rnd(n) for n in prob.n] for _ in range(s1.nterms)]
             bank.P.append(Pc)
         stepf = exprk3ds_step
     else:
