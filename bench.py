@@ -210,6 +210,44 @@ def setup_ctx(kx, prob, scheme, tau, stream):
     return ctx, time.perf_counter() - t0
 
 
+def other_configs(kx, torch, stream, steps=10):
+    """Secondary workloads reported beside the headline (same timing protocol, fewer steps):
+    C3 (3D FitzHugh-Nagumo 128^3, exprk3ds_real) and the complex split on C2."""
+    import inputs
+    out = {}
+    flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    for name, cfg_name, scheme in [("C3_fhn_128^3_etd3rkds_real", "C3", None),
+                                   ("C2_schnakenberg_1024^2_exprk3ds_cplx", "C2", "exprk3ds_cplx")]:
+        cfg = config_dict(cfg_name)
+        if scheme:
+            cfg["scheme"] = scheme
+        prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
+        tau = cfg["T"] / cfg["m"]
+        ctx, _ = setup_ctx(kx, prob, cfg["scheme"], tau, stream)
+        U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
+        for _ in range(3):
+            ctx.step(U)
+        ctx.sync()
+        ctx.set_profiling(True)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        with torch.cuda.stream(stream):
+            for k in range(steps):
+                flush.fill_(float(k))
+                ev[k][0].record()
+                ctx.step(U)
+                ev[k][1].record()
+        torch.cuda.synchronize()
+        prof = ctx.profile()
+        ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+        ach = prof["gemm_flops"] / prof["gemm_ms"] / 1e9
+        out[name] = {"steps_per_s": round(1e3 / ms, 2), "ms_per_step": round(ms, 4),
+                     "gemm_tflops": round(ach, 2)}
+        ctx.close()
+        del U
+        torch.cuda.empty_cache()
+    return out
+
+
 def tucker_sweep(kx, torch, stream, budget_s=25.0):
     """Tucker microbenchmark at a few sizes: dense flops / event time."""
     out = {}
@@ -347,6 +385,7 @@ def run_kx(args, rank, world, sharded):
         del U, flush
         torch.cuda.empty_cache()
         res["tucker"] = tucker_sweep(kx, torch, stream)
+        res["others"] = other_configs(kx, torch, stream)
     return res, cfg, prob
 
 
@@ -437,6 +476,7 @@ def main():
                        "h2d_bytes_per_step": res["e2e_bytes"], "d2h_bytes_per_step": res["e2e_bytes"]}
     if "tucker" in res:
         line["tucker_tflops"] = res["tucker"]
+        line["other_workloads"] = res.get("others")
         if peak:
             line["tucker_frac_of_dmma"] = {k: round(v / peak, 3) for k, v in res["tucker"].items()}
     if not args.no_extras and prob.N <= 64 * 1024 * 1024:
