@@ -121,60 +121,80 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------------------------- oracle --
-def oracle_sample(cfg_name, seconds):
-    """Time the CPU oracle's step function on this host (bounded sample).  Returns
-    (steps_per_s, cores, sample description)."""
-    import inputs
-    from oracle.etd import Exprk3Bank, exprk3ds_step, etd2rkds_step, Etd2Bank
-    from oracle import coeffs
-    from oracle.models import g_of
-    from oracle.tensor import unvec
-    cfg = config_dict(cfg_name)
-    prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
-    tau = cfg["T"] / cfg["m"]
-    d = cfg["d"]
-    rs = np.random.default_rng(0)
-    # phi-bank formation (setup, ~7 TFLOP for C2 in the oracle) is replaced by random dense
-    # matrices of the same shapes: the per-step cost does not depend on their values.
-    if cfg["scheme"] in ("etd3rkds", "exprk3ds_cplx"):
-        variant = "cplx" if cfg["scheme"] == "exprk3ds_cplx" else "real"
-        s1, s2 = coeffs.etd3_scheme(1, d, variant), coeffs.etd3_scheme(2, d, variant)
-        bank = Exprk3Bank(tau, s1, s2)
+class OracleRunner:
+    """The CPU oracle's step function on this host's cores, on the bench workload.  The
+    phi-bank formation (setup, ~7 TFLOP for C2 in the oracle) is replaced by random dense
+    matrices of the same shapes: the per-step cost does not depend on their values."""
 
-        def rnd(n):
-            m = rs.uniform(0, 1.0 / n, (n, n))
-            return m + 1j * rs.uniform(0, 1.0 / n, (n, n)) if variant == "cplx" else m
-        for c in range(2):
-            Pc = {}
-            for key in [("2", 1), ("3", 1), ("3", 2), ("f", 1), ("f", 2)]:
-                Pc[key] = [[rnd(n) for n in prob.n] for _ in range(s1.nterms)]
-            bank.P.append(Pc)
-        stepf = exprk3ds_step
-    else:
-        P = [[[rs.uniform(0, 1.0 / n, (n, n)) for n in prob.n]] for _ in range(2)]
-        bank = Etd2Bank(tau, P, P, 1.0, 2.0 ** (d - 1))
-        stepf = etd2rkds_step
-    g = g_of(prob.model)
-    U0 = [unvec(u, prob.n) for u in prob.U0]
-    t0 = time.perf_counter()
-    k = 0
-    while True:
+    def __init__(self, cfg_name):
+        import inputs
+        from oracle.etd import Exprk3Bank, exprk3ds_step, etd2rkds_step, Etd2Bank
+        from oracle import coeffs
+        from oracle.models import g_of
+        from oracle.tensor import unvec
+        cfg = config_dict(cfg_name)
+        self.cfg, self.cfg_name = cfg, cfg_name
+        prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
+        tau = cfg["T"] / cfg["m"]
+        d = cfg["d"]
+        rs = np.random.default_rng(0)
+        if cfg["scheme"] in ("etd3rkds", "exprk3ds_cplx"):
+            variant = "cplx" if cfg["scheme"] == "exprk3ds_cplx" else "real"
+            s1, s2 = coeffs.etd3_scheme(1, d, variant), coeffs.etd3_scheme(2, d, variant)
+            bank = Exprk3Bank(tau, s1, s2)
+
+            def rnd(n):
+                m = rs.uniform(0, 1.0 / n, (n, n))
+                return m + 1j * rs.uniform(0, 1.0 / n, (n, n)) if variant == "cplx" else m
+            for c in range(2):
+                Pc = {}
+                for key in [("2", 1), ("3", 1), ("3", 2), ("f", 1), ("f", 2)]:
+                    Pc[key] = [[rnd(n) for n in prob.n] for _ in range(s1.nterms)]
+                bank.P.append(Pc)
+            self.stepf = exprk3ds_step
+        else:
+            P = [[[rs.uniform(0, 1.0 / n, (n, n)) for n in prob.n]] for _ in range(2)]
+            bank = Etd2Bank(tau, P, P, 1.0, 2.0 ** (d - 1))
+            self.stepf = etd2rkds_step
+        self.bank, self.prob, self.g = bank, prob, g_of(prob.model)
+        self.U0 = [unvec(u, prob.n) for u in prob.U0]
+
+    def step(self):
         # every sampled step starts from the initial data (random P would otherwise let the
         # state overflow; the cost of a step does not depend on the values)
-        stepf(U0, 0.0, bank, prob.A, g, prob.params)
-        k += 1
-        if time.perf_counter() - t0 >= seconds:
-            break
-    el = time.perf_counter() - t0
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
-    sample = (f"{k} oracle {cfg['scheme']} step(s) of {cfg_name} ({cfg['desc']}), numpy fp64 "
-              f"(BLAS matmul per mode product) on {os.cpu_count()} host cores; phi-bank formation "
-              f"excluded (random dense P of the same shapes)")
-    return k / el, cores, sample
+        self.stepf(self.U0, 0.0, self.bank, self.prob.A, self.g, self.prob.params)
+
+    def sample(self, seconds):
+        """steps/s over >= 1 step and about `seconds` of CPU work."""
+        t0 = time.perf_counter()
+        k = 0
+        while True:
+            self.step()
+            k += 1
+            if time.perf_counter() - t0 >= seconds:
+                break
+        return k / (time.perf_counter() - t0), k
+
+    @staticmethod
+    def cores():
+        try:
+            from threadpoolctl import threadpool_info
+            return max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+        except Exception:
+            return os.cpu_count()
+
+    def describe(self, k):
+        c = self.cfg
+        return (f"{k} oracle {c['scheme']} step(s) of {self.cfg_name} ({c['desc']}), numpy fp64 "
+                f"(BLAS matmul per mode product) on {os.cpu_count()} host cores; phi-bank formation "
+                f"excluded (random dense P of the same shapes)")
+
+
+def oracle_sample(cfg_name, seconds):
+    """(steps_per_s, cores, sample description) of a bounded oracle sample."""
+    r = OracleRunner(cfg_name)
+    v, k = r.sample(seconds)
+    return v, r.cores(), r.describe(k)
 
 
 # -------------------------------------------------------------------------------- GPU arm --
@@ -400,18 +420,20 @@ def main():
         return 2
     cfg = config_dict(args.config)
     if args.impl == "reference":
+        # the oracle on this host's cores (rank 0 only under torchrun; the others exit 0)
         if rank != 0:
             return 0
-        for _ in range(args.warmup if args.warmup < 1 else 0):
-            pass
-        vals = []
-        cores = None
-        sample = ""
-        per = max(1.0, args.cpu_seconds / max(1, args.steps))
-        for k in range(max(1, args.steps)):
-            v, cores, sample = oracle_sample(args.config, per)
+        runner = OracleRunner(args.config)
+        for _ in range(args.warmup):        # untimed warm-up steps
+            runner.step()
+        per = max(0.5, args.cpu_seconds / max(1, args.steps))
+        vals, ks = [], 0
+        for _ in range(max(1, args.steps)):   # K timed samples, each >= 1 step
+            v, k = runner.sample(per)
             vals.append(v)
+            ks += k
         value = statistics.mean(vals)
+        cores = runner.cores()
         line = {"metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -419,7 +441,7 @@ def main():
                 "config": {"workload": f"{args.config}: {cfg['desc']}", "grid": [cfg["n"]] * cfg["d"],
                            "species": 2, "scheme": cfg["scheme"], "parallelism": "single host"},
                 "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores,
-                                 "kind": "oracle", "sample": sample},
+                                 "kind": "oracle", "sample": runner.describe(ks)},
                 "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
