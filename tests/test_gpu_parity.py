@@ -505,3 +505,19 @@ def test_complex_sharded_loopback(kx):
         assert relerr(vec(np.concatenate(parts, axis=-1)), U1[s].cpu().numpy()) <= 1e-13
     grp.close()
     one.close()
+
+
+@pytest.mark.parametrize("case", [("fhn", [6, 5, 4, 7], "etd3rkds", 0.015, 4),
+                                  ("fhn", [4, 3, 5, 2, 3], "etd3rkds", 0.01, 3),
+                                  ("schnakenberg", [5, 6, 4, 3], "etd2rkds", 1e-4, 4),
+                                  ("fhn", [8, 6, 4, 4], "exprk3ds_cplx", 0.01, 2),
+                                  ("schnakenberg", [40], "etd2rkds", 1e-4, 5)])
+def test_step_parity_other_dimensions(ctx, case):
+    """d = 1, 4, 5 (Table 3 carries 2^{d-3}; Table 2 2^{d-2}; middle modes mu = d-1..2)."""
+    model, n, scheme, tau, steps = case
+    prob = inputs.make_problem(model, len(n), n, seed=9)
+    setup_problem(ctx, prob, scheme, tau)
+    out = run_gpu(ctx, prob, scheme, tau, steps)
+    ref, _ = integrate(prob, scheme, T=tau * 10, m=10, steps=steps)
+    err = max(relerr(out[c], ref[c]) for c in range(2))
+    assert err <= 1e-10, err
