@@ -30,6 +30,7 @@ for scheme in sys.argv[1:] or ["etd3rkds"]:
         for _ in range(3):
             ctx.step(U)
         ctx.sync()
+        ctx.reset_counters()
         ts = []
         for k in range(20):
             with torch.cuda.stream(s):
