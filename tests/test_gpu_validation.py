@@ -102,3 +102,53 @@ def test_full_integration_parity(kx, case):
     ref, _ = integrate(prob, scheme, T=T, m=m)
     err = max(np.max(np.abs(out[c] - ref[c])) / np.max(np.abs(ref[c])) for c in range(2))
     assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("case", [("C2", 2), ("C3", 3)])
+def test_full_size_config_steps(kx, case):
+    """BASELINE.json configs[1] (1024^2 Schnakenberg) and configs[2] (128^3 FHN) at their full
+    size, in the launch configuration bench.py times (graph replay), vs the oracle — whose
+    phi-bank at n = 1024 alone is ~5 TFLOP on the host (~30 s)."""
+    from oracle.etd import integrate
+    name, steps = case
+    cfg = inputs.CONFIGS[name]
+    prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
+    out = integrate_gpu(kx, prob, cfg["scheme"], cfg["T"] * steps / cfg["m"], steps)
+    ref, _ = integrate(prob, cfg["scheme"], T=cfg["T"], m=cfg["m"], steps=steps)
+    err = max(np.max(np.abs(out[c] - ref[c])) / np.max(np.abs(ref[c])) for c in range(2))
+    assert err <= 1e-10, err
+
+
+@pytest.mark.parametrize("scheme", ["etd3rkds", "exprk3ds_cplx"])
+def test_c4_size_linear_closed_form(kx, scheme):
+    """configs[3] size (512^3 FHN delta_v, tau = 0.015), g = 0, cosine-mode data: one step is
+    the scalar recurrence of SURVEY §8(c) (no oracle run needed at this size)."""
+    from oracle import coeffs
+    n, delta, tau = 512, 42.1887, 0.015
+    A = inputs.laplacian_neumann(n, math.pi, delta)
+    ks = (2, 37, 130)
+    x = inputs.kron_vec([inputs.cosine_mode(n, k) for k in ks])
+    lams = [inputs.cosine_eigenvalue(n, math.pi, delta, k) for k in ks]
+    ctx = kx.Context(0)
+    ctx.set_grid([n, n, n], 2)
+    for c in range(2):
+        for mu in (1, 2, 3):
+            ctx.set_direction_matrix(c, mu, A)
+    ctx.set_model("none")
+    ctx.set_tau(tau, scheme)
+    U = [torch.from_numpy(x).cuda(), torch.from_numpy(x).cuda()]
+    ctx.step(U)
+    ctx.sync()
+    s = coeffs.table3(1, 3) if scheme == "etd3rkds" else coeffs.table2(1, 3)
+
+    def phis(ell, z):
+        import cmath
+        e = cmath.exp(z)
+        return [e, (e - 1) / z, (e - 1 - z) / (z * z)][ell]
+
+    split = sum(eta * np.prod([phis(li, tau * al[m] * lams[m]) for m in range(3)])
+                for eta, li, al in zip(s.etas, s.inner, s.alphas))
+    expect = np.real(1.0 + tau * sum(lams) * split) * x
+    got = U[0].cpu().numpy()
+    assert np.max(np.abs(got - expect)) / np.max(np.abs(expect)) <= 1e-11
+    ctx.close()
