@@ -377,7 +377,9 @@ def run_kx(args, rank, world, sharded):
     clocks = ClockSampler(rank % max(1, torch.cuda.device_count()))
     clocks.start()
     time.sleep(0.3)
+    torch.cuda.profiler.start()    # `ncu --profile-from-start off` sees exactly the timed steps
     step_ms = timed_pass(False)
+    torch.cuda.profiler.stop()
     clk = clocks.stop()
     cnt = ctx.counters()
     # timed region 2: the same K steps with an event pair around every kernel (the graph's
