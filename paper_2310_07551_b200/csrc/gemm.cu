@@ -45,6 +45,31 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// arrives on `bar` once all of this thread's prior cp.async operations have completed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col); fragments: a = A[g][t], b = B[t][g],
 // c = {C[g][2t], C[g][2t+1]} with g = lane/4, t = lane%4.
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -61,7 +86,7 @@ struct Cfg {
   static constexpr int A_ST = AROW ? BM * SA : BK * SA;
   static constexpr int SB = BN + 4;
   static constexpr int B_ST = BK * SB;
-  static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8;
+  static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8 + 2 * STAGES * 8;   // + mbarriers
   // loader geometry: chunks of VEC doubles, each thread owns IA (A) and IB (B) chunks
   static constexpr int CPR_A = AROW ? BK / VEC : BM / VEC;   // chunks per smem row of A
   static constexpr int IA = BM * BK / VEC / NT;
@@ -310,32 +335,50 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   const int wm0 = (warp / T_::C_::WARPS_N) * WM, wn0 = (warp % T_::C_::WARPS_N) * WN;
   const int cta = blockIdx.x;
 
+  // Pipeline synchronisation with mbarriers instead of a CTA barrier per k-tile:
+  //   full[s]  — every thread's cp.async into stage s has landed (cp.async.mbarrier.arrive)
+  //   empty[s] — every thread has finished reading stage s
+  // so a warp may run ahead into the next k-tile as soon as its data is there.
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * B_ST);
+  uint64_t* empty = full + STAGES;
+  if (tid == 0) {
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(full + st, NT);
+      mbar_init(empty + st, NT);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
   // ---- producer
   WorkIter pit;
   pit.init(sc, cta);
   Seg ps;
   bool p_ok = pit.next(ps);
   int pk = 0;
+  int pkt = 0;   // k-tiles issued so far (stage = pkt % STAGES, fill = pkt / STAGES)
   typename T_::Loader ld;
   if (p_ok) {
     pk = ps.kb;
     ld.setup(p, T_::coords(p, sc, ps.tl), ps.kb);
   }
-  auto produce = [&](int stage) {
-    if (p_ok) {
-      ld.issue(p, As + stage * A_ST, Bs + stage * B_ST);
-      if (++pk == ps.ke) {
-        p_ok = pit.next(ps);
-        if (p_ok) {
-          pk = ps.kb;
-          ld.setup(p, T_::coords(p, sc, ps.tl), ps.kb);
-        }
+  auto produce = [&]() {
+    if (!p_ok) return;
+    const int stage = pkt % STAGES, fill = pkt / STAGES;
+    if (fill > 0) mbar_wait(empty + stage, (fill - 1) & 1);
+    ld.issue(p, As + stage * A_ST, Bs + stage * B_ST);
+    cp_async_mbar_arrive(full + stage);
+    ++pkt;
+    if (++pk == ps.ke) {
+      p_ok = pit.next(ps);
+      if (p_ok) {
+        pk = ps.kb;
+        ld.setup(p, T_::coords(p, sc, ps.tl), ps.kb);
       }
     }
-    cp_async_commit();
   };
 #pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) produce(st);
+  for (int st = 0; st < STAGES - 1; ++st) produce();
 
   // ---- consumer
   WorkIter cit;
@@ -347,14 +390,14 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     return;
   }
   int ck = cs.kb;
+  int ckt = 0;   // k-tiles consumed so far
   Coord cd = T_::coords(p, sc, cs.tl);
   double acc[FM][FN][2];
   T_::zero(acc);
-  int stage_c = 0, stage_p = STAGES - 1;
   double* ws_me = p.sk_ws + (size_t)cta * (FM * FN * 2 * NT);
   while (true) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
+    const int stage_c = ckt % STAGES;
+    mbar_wait(full + stage_c, (ckt / STAGES) & 1);
     const double* as = As + stage_c * A_ST;
     const double* bs = Bs + stage_c * B_ST;
 #pragma unroll
@@ -371,10 +414,10 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
       for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-      if (kk == 0) produce(stage_p);   // overlaps the DMMAs queued for this k-step
+      if (kk == 0) produce();   // overlaps the DMMAs queued for this k-step
     }
-    stage_c = stage_c + 1 == STAGES ? 0 : stage_c + 1;
-    stage_p = stage_p + 1 == STAGES ? 0 : stage_p + 1;
+    mbar_arrive(empty + stage_c);
+    ++ckt;
     if (++ck < cs.ke) continue;
 
     // ---- segment finished
