@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--no-extras", action="store_true", help="skip Tucker sweep / e2e / cpu leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="sharded mode: one exchange per phase instead of term-by-term overlap")
     ap.add_argument("--scheme", default=None, choices=["etd2rkds", "etd3rkds", "exprk3ds_cplx"],
                     help="override the config's scheme (e.g. the complex split, Table 2)")
     ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "sharded"],
@@ -329,6 +331,8 @@ def run_kx(args, rank, world, sharded):
             dist.broadcast_object_list(uid, src=0)
         prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0, slab=(rank, world))
         ctx = kx.Context(torch.cuda.current_device(), stream, dist=(uid[0], rank, world))
+        if args.no_overlap:
+            ctx.set_dist_overlap(False)
         ctx.set_grid(prob.n, 2)
         for c in range(2):
             for mu in range(prob.d):

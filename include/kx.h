@@ -152,6 +152,10 @@ kx_status kx_create_dist(kx_ctx **ctx, int device, void *cuda_stream, const void
  * Used to test the sharded schedule on a single GPU.  U holds nranks*ncomp device pointers,
  * rank-major (U[r*ncomp + c]). */
 kx_status kx_create_group(kx_ctx **ctxs, int nranks, int device, void *cuda_stream);
+/* NCCL ranks (default: on when nranks > 1): the 3T + T + T term slots of each step are sent to the peers term
+ * by term on an internal communication stream while the next term's mode products run
+ * (SURVEY §8(f) f2); off = one exchange per phase on the context stream. */
+kx_status kx_set_dist_overlap(kx_ctx *ctx, int on);
 kx_status kx_step_group(kx_ctx *const *ctxs, int nranks, double t, double *const *U);
 
 /* ---------------------------------------------------------------- utilities -------- */

@@ -135,6 +135,11 @@ struct kx_ctx {
   // dist = 2 member of an in-process loopback group (exchanges are device copies)
   int dist = 0, rank = 0, nranks = 1;
   void* nccl_comm = nullptr;
+  // f2: term-by-term exchange overlapped with the remaining terms' mode products (NCCL ranks)
+  int overlap = 1;
+  cudaStream_t comm = nullptr;
+  cudaEvent_t ev_term[64] = {};
+  cudaEvent_t ev_join = nullptr;
   long long nA[KX_MAXD] = {};    // local extents, layout A: i_d sharded (n_d / P)
   long long nB[KX_MAXD] = {};    // local extents, layout B: i_1 sharded (n_1 / P)
   long long Nloc = 0;
@@ -1221,10 +1226,36 @@ kx_status dist_f_build(kx_ctx* c) {
 }
 
 // [B] first + middle modes of group gi on X_B; the term slots go back to layout A
+kx_status nccl_exchange(kx_ctx* c, const Exchange& x, cudaStream_t st);
+
 kx_status dist_group(kx_ctx* c, int gi, double* const* Xb, Exchange& x) {
   set_layout(c, true);
   const Group& G = c->groups[gi];
   double* const* ws = nullptr;
+  if (c->dist == 1 && c->overlap && c->comm) {
+    // f2: modes d..2 term by term; each term's slots go to the peers on the comm stream while
+    // the next term's mode products run; the compute stream joins before the stage GEMM
+    const int pl = c->cplx ? 2 : 1;
+    const int nterm = G.nterms / pl;
+    if (nterm > 64) return fail(c, KX_ERR_UNSUPPORTED, "too many terms");
+    for (int t = 0; t < nterm; ++t) {
+      KX_TRY(group_modes(c, G, t * pl, pl, Xb, G.slot0 + t * pl, &ws));
+      KX_CUDA(c, cudaEventRecord(c->ev_term[t], c->cur));
+      KX_CUDA(c, cudaStreamWaitEvent(c->comm, c->ev_term[t], 0));
+      Exchange xt;
+      xt.count = (size_t)(c->Nloc / c->nranks);
+      for (int k = 0; k < pl; ++k)
+        for (int s = 0; s < c->ncomp; ++s) {
+          const long long slot = G.slot0 + t * pl + k;
+          xt.add(ws[s] + slot * c->Nloc, c->RA[s] + slot * c->Nloc);
+        }
+      KX_TRY(nccl_exchange(c, xt, c->comm));
+    }
+    KX_CUDA(c, cudaEventRecord(c->ev_join, c->comm));
+    KX_CUDA(c, cudaStreamWaitEvent(c->cur, c->ev_join, 0));
+    x = Exchange{};
+    return KX_OK;
+  }
   KX_TRY(group_modes(c, G, 0, G.nterms, Xb, G.slot0, &ws));
   x.count = (size_t)(c->Nloc / c->nranks);
   for (int t = 0; t < G.nterms; ++t)
@@ -1323,7 +1354,7 @@ kx_status dist_phase(kx_ctx* c, double* const* U, int ph, Exchange& x) {
   return fail(c, KX_ERR_INVALID, "bad phase");
 }
 
-kx_status nccl_exchange(kx_ctx* c, const Exchange& x) {
+kx_status nccl_exchange(kx_ctx* c, const Exchange& x, cudaStream_t st) {
 #ifdef KX_HAVE_NCCL
   NcclApi& api = nccl();
   ncclComm_t comm = static_cast<ncclComm_t>(c->nccl_comm);
@@ -1334,8 +1365,8 @@ kx_status nccl_exchange(kx_ctx* c, const Exchange& x) {
   KX_TRY(chk(api.GroupStart()));
   for (int k = 0; k < x.nbuf; ++k)
     for (int q = 0; q < c->nranks; ++q) {
-      KX_TRY(chk(api.Send(x.send[k] + q * x.count, x.count, ncclFloat64, q, comm, c->cur)));
-      KX_TRY(chk(api.Recv(x.recv[k] + q * x.count, x.count, ncclFloat64, q, comm, c->cur)));
+      KX_TRY(chk(api.Send(x.send[k] + q * x.count, x.count, ncclFloat64, q, comm, st)));
+      KX_TRY(chk(api.Recv(x.recv[k] + q * x.count, x.count, ncclFloat64, q, comm, st)));
     }
   KX_TRY(chk(api.GroupEnd()));
   return KX_OK;
@@ -1350,7 +1381,7 @@ kx_status dist_step_nccl(kx_ctx* c, double* const* U) {
   Exchange x;
   for (int ph = 0; ph < dist_phases(c); ++ph) {
     KX_TRY(dist_phase(c, U, ph, x));
-    if (x.nbuf) KX_TRY(nccl_exchange(c, x));
+    if (x.nbuf) KX_TRY(nccl_exchange(c, x, c->cur));
   }
   c->cnt.steps += 1;
   return KX_OK;
@@ -1425,6 +1456,10 @@ void kx_destroy(kx_ctx* c) {
 #ifdef KX_HAVE_NCCL
   if (c->nccl_comm && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
 #endif
+  if (c->comm) cudaStreamDestroy(c->comm);
+  for (auto e : c->ev_term)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->sk_ws) cudaFree(c->sk_ws);
   if (c->sk_flags) cudaFree(c->sk_flags);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -1637,6 +1672,12 @@ kx_status kx_kronsum(kx_ctx* c, int comp, const double* X, double* Y, double bet
   double* Ys[1] = {Y};
   const double* Ds[1] = {Y};
   return kronsum_multi(c, comp, 1, Xs, Ys, beta, Ds);
+}
+
+kx_status kx_set_dist_overlap(kx_ctx* c, int on) {
+  if (!c) return KX_ERR_INVALID;
+  c->overlap = on != 0;
+  return KX_OK;
 }
 
 kx_status kx_set_kronsum_mode(kx_ctx* c, int mode) {
@@ -1858,6 +1899,10 @@ kx_status kx_create_dist(kx_ctx** out, int device, void* cuda_stream, const void
   }
   c->nccl_comm = comm;
   c->dist = 1;
+  c->overlap = nranks > 1;   // with one rank there is nothing to hide (self-copies only)
+  if (cudaStreamCreateWithFlags(&c->comm, cudaStreamNonBlocking) != cudaSuccess) c->comm = nullptr;
+  for (auto& e : c->ev_term) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   c->rank = rank;
   c->nranks = nranks;
   return KX_OK;

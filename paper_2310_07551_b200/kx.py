@@ -66,6 +66,7 @@ _SIGS = {
     "kx_create_dist": (_i, [C.POINTER(_vp), _i, _vp, _vp, _i, _i]),
     "kx_create_group": (_i, [C.POINTER(_vp), _i, _i, _vp]),
     "kx_step_group": (_i, [C.POINTER(_vp), _i, _d, C.POINTER(_vp)]),
+    "kx_set_dist_overlap": (_i, [_vp, _i]),
     "kx_get_counters": (_i, [_vp, C.POINTER(kx_counters)]),
     "kx_reset_counters": (_i, [_vp]),
     "kx_sync": (_i, [_vp]),
@@ -212,6 +213,9 @@ class Context:
 
     def kronsum(self, comp: int, X, Y, beta=0.0):
         self._check(kx_kronsum(self.h, comp, _ptr(X), _ptr(Y), beta))
+
+    def set_dist_overlap(self, on: bool):
+        self._check(kx_set_dist_overlap(self.h, 1 if on else 0))
 
     def set_kronsum_mode(self, dense: bool):
         self._check(kx_set_kronsum_mode(self.h, 1 if dense else 0))

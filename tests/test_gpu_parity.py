@@ -383,16 +383,20 @@ def test_sharded_step_loopback(kx, case):
     one.close()
 
 
-def test_nccl_single_rank_dist_context(kx):
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("scheme", ["etd3rkds", "exprk3ds_cplx"])
+def test_nccl_single_rank_dist_context(kx, overlap, scheme):
     """kx_create_dist with one rank (NCCL self-exchange): the distributed code path end to
-    end through NCCL on one GPU, equal to the single-GPU step to rounding."""
+    end through NCCL on one GPU, with and without the term-by-term overlapped exchange (f2),
+    equal to the single-GPU step to rounding."""
     prob = inputs.make_problem("fhn", 3, [16, 12, 8], seed=7)
     tau = 0.015
     uid = kx.nccl_unique_id()
     dctx = kx.Context(0, dist=(uid, 0, 1))
-    setup_problem(dctx, prob, "etd3rkds", tau)
+    dctx.set_dist_overlap(overlap)
+    setup_problem(dctx, prob, scheme, tau)
     one = kx.Context(0)
-    setup_problem(one, prob, "etd3rkds", tau)
+    setup_problem(one, prob, scheme, tau)
     Ud = [dev(u) for u in prob.U0]
     U1 = [dev(u) for u in prob.U0]
     for _ in range(3):
