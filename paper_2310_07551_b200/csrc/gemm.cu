@@ -535,16 +535,16 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
 template <bool AROW, int VEC>
 cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
   switch (which) {
-    case 0: return launch_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>(g, nz, stream);
-    case 1: return launch_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>(g, nz, stream);
+    case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>(g, nz, stream);
+    case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
     default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
   }
 }
 
 template <bool AROW, int VEC>
 void prepare_layout() {
-  prepare_cfg<128, 128, 32, 64, 32, AROW, VEC, 3>();
-  prepare_cfg<128, 64, 16, 64, 32, AROW, VEC, 3>();
+  prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>();
+  prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>();
   prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>();
 }
 
