@@ -525,3 +525,23 @@ def test_step_parity_other_dimensions(ctx, case):
     ref, _ = integrate(prob, scheme, T=tau * 10, m=10, steps=steps)
     err = max(relerr(out[c], ref[c]) for c in range(2))
     assert err <= 1e-10, err
+
+
+def test_out_of_memory_is_reported(ctx, kx):
+    """A grid whose exprk3ds workspaces exceed HBM (1024^3: ~0.4 TB) fails with KX_ERR_NOMEM at
+    kx_set_tau, frees what it allocated, and the context stays usable."""
+    n = [1024, 1024, 1024]
+    ctx.set_grid(n, 2)
+    A = inputs.laplacian_neumann(1024, math.pi, 1.0)
+    for c in range(2):
+        for mu in (1, 2, 3):
+            ctx.set_direction_matrix(c, mu, A)
+    with pytest.raises(kx.KxError) as ei:
+        ctx.set_tau(0.015, "etd3rkds")
+    assert ei.value.status == kx.KX_ERR_NOMEM
+    ctx.set_grid([16, 16], 1)
+    X = dev(tensor([16, 16], 1))
+    Y = dev(np.zeros(256))
+    ctx.tucker(X, Y, [dmat(np.eye(16)), dmat(np.eye(16))])
+    ctx.sync()
+    assert torch.equal(X, Y)
