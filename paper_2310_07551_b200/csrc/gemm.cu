@@ -528,6 +528,21 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
       sc.G_sk = (int)std::min<long long>(Gmax, sc.sk_units / 4);
     }
   }
+  if (sc.sk_units > 0) {
+    // stream-K CTAs wait on each other: a cooperative launch guarantees that the whole grid is
+    // co-resident even when other kernels share the GPU (otherwise the driver refuses it)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sc.G);
+    cfg.blockDim = dim3(C_::NT);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>, g, sc);
+  }
   gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc);
   return cudaGetLastError();
 }
