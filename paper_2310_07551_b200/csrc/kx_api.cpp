@@ -569,9 +569,20 @@ kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const
   std::vector<Exchange> xs(nranks);
   for (int ph = 0; ph < dist_phases(ctxs[0]); ++ph) {
     for (int r = 0; r < nranks; ++r) KX_TRY(dist_phase(ctxs[r], U + (size_t)r * nc, ph, xs[r]));
-    // loopback all-to-all: device copies on the shared stream, after every rank's phase
+    // loopback exchanges: device copies on the shared stream, after every rank's phase
     for (int r = 0; r < nranks; ++r) {
       const Exchange& xr = xs[r];
+      if (xr.kind == 1) {   // halo: first plane -> rank-1's upper halo, last plane -> rank+1's lower
+        for (int k = 0; k + 1 < xr.nbuf; k += 2) {
+          if (r > 0)
+            KX_CUDA(ctxs[r], cudaMemcpyAsync(xs[r - 1].recv[k + 1], xr.send[k], xr.count * 8,
+                                             cudaMemcpyDeviceToDevice, ctxs[r]->stream));
+          if (r + 1 < nranks)
+            KX_CUDA(ctxs[r], cudaMemcpyAsync(xs[r + 1].recv[k], xr.send[k + 1], xr.count * 8,
+                                             cudaMemcpyDeviceToDevice, ctxs[r]->stream));
+        }
+        continue;
+      }
       for (int k = 0; k < xr.nbuf; ++k)
         for (int q = 0; q < nranks; ++q)
           KX_CUDA(ctxs[r], cudaMemcpyAsync(xs[q].recv[k] + (size_t)r * xr.count, xr.send[k] + (size_t)q * xr.count,

@@ -391,6 +391,10 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
       KX_TRY(wal(&c->F_B[comp], N));
       KX_TRY(wal(&c->D_pack[comp], N));
       KX_TRY(wal(&c->D_B[comp], N));
+      KX_TRY(wal(&c->F_pack[comp], N));
+      const size_t plane = N / (size_t)c->nA[d - 1];
+      KX_TRY(wal(&c->halo_lo[comp], plane));
+      KX_TRY(wal(&c->halo_hi[comp], plane));
     }
   }
   KX_CUDA(c, cudaStreamSynchronize(c->cur));

@@ -89,6 +89,7 @@ void drop_bank(kx_ctx* c) {
     c->G[s] = c->F[s] = c->D[s] = c->Us[s] = c->W1[s] = c->W2[s] = nullptr;
     c->RA[s] = c->T1G_pack[s] = c->U_pack[s] = c->T1G_B[s] = c->U_B[s] = c->F_B[s] = nullptr;
     c->D_pack[s] = c->D_B[s] = nullptr;
+    c->halo_lo[s] = c->halo_hi[s] = c->F_pack[s] = nullptr;
   }
 }
 

@@ -154,6 +154,9 @@ struct kx_ctx {
   double* F_B[MAXS] = {};
   double* D_pack[MAXS] = {};
   double* D_B[MAXS] = {};
+  double* halo_lo[MAXS] = {};   // tridiagonal K on a slab: the neighbours' boundary planes of U
+  double* halo_hi[MAXS] = {};
+  double* F_pack[MAXS] = {};
 
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -254,7 +257,11 @@ struct NcclApi {
 NcclApi& nccl();   // dlopen'ed once (the NCCL torch already loaded)
 // Buffers one rank exchanges after a phase: for k < nbuf, chunk q (count doubles) of send[k]
 // goes to rank q, which stores it at chunk `rank` of its recv[k].
+// kind 0: all-to-all (above).  kind 1: halo — for each component s, send[2s] (this rank's
+// first plane) goes to rank-1 and lands in its recv[2s+1]; send[2s+1] (last plane) goes to
+// rank+1 and lands in its recv[2s]; the global end ranks skip the missing side.
 struct Exchange {
+  int kind = 0;
   int nbuf = 0;
   size_t count = 0;
   const double* send[64];
@@ -268,6 +275,7 @@ struct Exchange {
 void set_layout(kx_ctx* c, bool B);
 kx_status dist_f_source(kx_ctx* c, double* const* U, Exchange& x);
 kx_status dist_f_build(kx_ctx* c);
+bool dist_banded(const kx_ctx* c);
 kx_status dist_group(kx_ctx* c, int gi, double* const* Xb, Exchange& x);
 kx_status dist_stage(kx_ctx* c, const Stage& S, double* const* out, const double* const* addend);
 kx_status dist_d_source(kx_ctx* c, Exchange& x);

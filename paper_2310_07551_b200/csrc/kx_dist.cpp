@@ -205,7 +205,65 @@ kx_status dist_d_source(kx_ctx* c, Exchange& x) {
   return KX_OK;
 }
 
-int dist_phases(const kx_ctx* c) { return c->scheme == KX_ETD2RKDS ? 5 : 7; }
+// Tridiagonal A_mu (the FD Laplacians of Sec. 3): the Kronecker sum is a stencil; on a slab
+// only the two boundary planes of U cross ranks (a halo exchange with the neighbours), and F is
+// formed locally in layout A and written peer-packed — one all-to-all instead of two, and no
+// dense Kronecker-sum mode products.
+bool dist_banded(const kx_ctx* c) { return all_tridiag(c, 0, c->ncomp); }
+
+// [A] G = g(U); the boundary planes of U go to the neighbouring ranks
+kx_status dist_f_halo(kx_ctx* c, double* const* U, Exchange& x) {
+  set_layout(c, false);
+  KX_TRY(nonlin(c, 0, U, c->G));
+  const long long ndl = c->nA[c->d - 1];
+  const long long plane = c->Nloc / ndl;
+  x.kind = 1;
+  x.count = (size_t)plane;
+  for (int s = 0; s < c->ncomp; ++s) {
+    x.add(U[s], c->halo_lo[s]);
+    x.add(U[s] + (ndl - 1) * plane, c->halo_hi[s]);
+  }
+  return KX_OK;
+}
+
+// [A] F = G + sum_mu U x_mu A_mu (stencil, halos for the sharded direction), peer-packed
+kx_status dist_f_stencil(kx_ctx* c, double* const* U, Exchange& x) {
+  set_layout(c, false);
+  kx::StencilArgs a;
+  a.d = c->d;
+  a.ns = c->ncomp;
+  a.N = c->Nloc;
+  a.beta = 1.0;
+  for (int mu = 0; mu < c->d; ++mu) a.n[mu] = c->nA[mu];
+  a.d_off = (long long)c->rank * c->nA[c->d - 1];
+  a.n_glob_d = c->n[c->d - 1];
+  a.pack_n1 = c->n[0];
+  a.pack_n1l = c->n[0] / c->nranks;
+  for (int s = 0; s < c->ncomp; ++s) {
+    a.X[s] = U[s];
+    a.Y[s] = c->F_pack[s];
+    a.Dd[s] = c->G[s];
+    a.halo_lo[s] = c->halo_lo[s];
+    a.halo_hi[s] = c->halo_hi[s];
+    for (int mu = 0; mu < c->d; ++mu) {
+      const double* t = c->A_tri[s][mu];
+      const long long n = c->n[mu];
+      a.lo[s][mu] = t;
+      a.di[s][mu] = t + n;
+      a.up[s][mu] = t + 2 * n;
+    }
+  }
+  KX_TRY(run_other(c, [&] { return kx::launch_kronsum_tridiag(a, c->cur); }));
+  c->cnt.mode_products += (long long)c->ncomp * c->d;
+  c->cnt.kronsum_actions += c->ncomp;
+  x.count = (size_t)(c->Nloc / c->nranks);
+  for (int s = 0; s < c->ncomp; ++s) x.add(c->F_pack[s], c->F_B[s]);
+  return KX_OK;
+}
+
+int dist_phases(const kx_ctx* c) {
+  return (c->scheme == KX_ETD2RKDS ? 5 : 7) + (dist_banded(c) ? 1 : 0);
+}
 
 kx_status dist_phase(kx_ctx* c, double* const* U, int ph, Exchange& x) {
   x = Exchange{};
@@ -215,6 +273,12 @@ kx_status dist_phase(kx_ctx* c, double* const* U, int ph, Exchange& x) {
   for (int s = 0; s < c->ncomp; ++s) {
     Uc[s] = U[s];
     Usc[s] = c->Us[s];
+  }
+  if (dist_banded(c)) {
+    if (ph == 0) return dist_f_halo(c, U, x);
+    if (ph == 1) return dist_f_stencil(c, U, x);
+    if (ph == 2) return dist_group(c, 0, c->F_B, x);
+    ph -= 1;   // the remaining phases are those of the dense schedule
   }
   switch (ph) {
     case 0: return dist_f_source(c, U, x);
@@ -251,6 +315,20 @@ kx_status nccl_exchange(kx_ctx* c, const Exchange& x, cudaStream_t st) {
     return KX_OK;
   };
   KX_TRY(chk(api.GroupStart()));
+  if (x.kind == 1) {
+    for (int k = 0; k + 1 < x.nbuf; k += 2) {
+      if (c->rank > 0) {
+        KX_TRY(chk(api.Send(x.send[k], x.count, ncclFloat64, c->rank - 1, comm, st)));
+        KX_TRY(chk(api.Recv(x.recv[k], x.count, ncclFloat64, c->rank - 1, comm, st)));
+      }
+      if (c->rank + 1 < c->nranks) {
+        KX_TRY(chk(api.Send(x.send[k + 1], x.count, ncclFloat64, c->rank + 1, comm, st)));
+        KX_TRY(chk(api.Recv(x.recv[k + 1], x.count, ncclFloat64, c->rank + 1, comm, st)));
+      }
+    }
+    KX_TRY(chk(api.GroupEnd()));
+    return KX_OK;
+  }
   for (int k = 0; k < x.nbuf; ++k)
     for (int q = 0; q < c->nranks; ++q) {
       KX_TRY(chk(api.Send(x.send[k] + q * x.count, x.count, ncclFloat64, q, comm, st)));

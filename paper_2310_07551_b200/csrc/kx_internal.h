@@ -77,6 +77,13 @@ struct StencilArgs {
   const double* di[MAXS][6] = {};
   const double* up[MAXS][6] = {};
   double beta = 0.0;
+  // distributed slab (layout A): the local i_d range starts at global index d_off of n_glob_d;
+  // halo_lo/halo_hi hold the neighbouring ranks' boundary planes (null at the global ends)
+  long long d_off = 0, n_glob_d = 0;
+  const double* halo_lo[MAXS] = {};
+  const double* halo_hi[MAXS] = {};
+  // optional peer-packed output, as PointwiseArgs::pack_*
+  long long pack_n1 = 0, pack_n1l = 0;
 };
 cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream);
 

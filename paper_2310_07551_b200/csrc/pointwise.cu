@@ -162,10 +162,20 @@ __global__ void __launch_bounds__(256) kronsum_tridiag_kernel(const StencilArgs 
       for (int mu = 5; mu >= 1; --mu) {
         if (mu < a.d) {
           const long long i = idx[mu], nm = a.n[mu], st = str[mu];
-          double t = a.di[s][mu][i] * X[p];
-          if (i > 0) t = fma(a.lo[s][mu][i], X[p - st], t);
-          if (i + 1 < nm) t = fma(a.up[s][mu][i], X[p + st], t);
-          acc += t;
+          if (mu == a.d - 1 && a.n_glob_d) {
+            // sharded last direction: global index, neighbour planes from the halos
+            const long long ig = i + a.d_off;
+            const long long pp = p - i * st;   // offset inside the plane
+            double t = a.di[s][mu][ig] * X[p];
+            if (ig > 0) t = fma(a.lo[s][mu][ig], i > 0 ? X[p - st] : a.halo_lo[s][pp], t);
+            if (ig + 1 < a.n_glob_d) t = fma(a.up[s][mu][ig], i + 1 < nm ? X[p + st] : a.halo_hi[s][pp], t);
+            acc += t;
+          } else {
+            double t = a.di[s][mu][i] * X[p];
+            if (i > 0) t = fma(a.lo[s][mu][i], X[p - st], t);
+            if (i + 1 < nm) t = fma(a.up[s][mu][i], X[p + st], t);
+            acc += t;
+          }
         }
       }
       {
@@ -174,7 +184,12 @@ __global__ void __launch_bounds__(256) kronsum_tridiag_kernel(const StencilArgs 
         if (i1 + 1 < n1) t = fma(a.up[s][0][i1], X[p + 1], t);
         acc += t;
       }
-      Y[p] = acc;
+      long long o = p;
+      if (a.pack_n1l) {   // peer-packed output (distributed contexts)
+        const long long q = i1 / a.pack_n1l;
+        o = q * (a.N / n1 * a.pack_n1l) + line * a.pack_n1l + (i1 - q * a.pack_n1l);
+      }
+      Y[o] = acc;
     }
   }
 }

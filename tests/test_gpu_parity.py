@@ -349,10 +349,12 @@ def slab(u, n, r, P):
                                   ("fhn", 3, [16, 16, 16], "etd3rkds", 0.015, 4),
                                   ("schnakenberg", 2, [64, 64], "etd2rkds", 0.25 / 3000, 4),
                                   ("fhn", 3, [16, 12, 8], "etd2rkds", 0.01, 2)])
-def test_sharded_step_loopback(kx, case):
+@pytest.mark.parametrize("dense_kronsum", [False, True], ids=["halo-stencil", "dense-kronsum"])
+def test_sharded_step_loopback(kx, case, dense_kronsum):
     """The slab-sharded schedule (layouts A/B, peer-packed all-to-alls, concat-K over
-    (term, source rank) segments) on an in-process loopback group: equals the single-GPU step
-    to rounding and the oracle to 1e-10."""
+    (term, source rank) segments; the Kronecker sum either as a stencil with a halo exchange
+    of the boundary planes or as dense mode products across layouts) on an in-process loopback
+    group: equals the single-GPU step to rounding and the oracle to 1e-10."""
     model, d, n, scheme, tau, P = case
     prob = inputs.make_problem(model, d, n, seed=5)
     one = kx.Context(0)
@@ -361,6 +363,7 @@ def test_sharded_step_loopback(kx, case):
     grp = kx.Group(P)
     for c in grp.ctx:
         setup_problem(c, prob, scheme, tau)
+        c.set_kronsum_mode(dense_kronsum)
     Ug = [[dev(slab(prob.U0[s], n, r, P)) for s in range(2)] for r in range(P)]
     steps = 3
     for k in range(steps):
