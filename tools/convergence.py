@@ -63,15 +63,19 @@ PROTOCOLS = [
 
 def main():
     quick = "--quick" in sys.argv
+    fhn_amp = float(sys.argv[sys.argv.index("--fhn-amp") + 1]) if "--fhn-amp" in sys.argv else None
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     out = {"note": "initial data are seeded (SplitMix64, seed 0) while the paper's were unseeded "
                    "U(0,1) draws: compare magnitudes and slopes, not digits"}
     for name, model, d, n, T, mref, ladders, paper in PROTOCOLS:
-        if quick and n > 150:
+        if (quick and n > 150) or (only and only not in name):
             continue
-        prob = inputs.make_problem(model, d, n, seed=0)
+        amp = fhn_amp if model == "fhn" else None
+        prob = inputs.make_problem(model, d, n, seed=0, amplitude=amp)
         ref, ref_rate = run(prob, "exprk3ds_real", T, mref)
+        refmax = float(max(np.max(np.abs(ref[c])) for c in range(2)))
         res = {"reference": {"scheme": "exprk3ds_real", "steps": mref, "steps_per_s": round(ref_rate, 1),
-                             "max_abs_u": float(np.max(np.abs(ref[0])))}, "paper": paper}
+                             "max_abs": refmax}, "paper": paper}
         for scheme, ladder in ladders.items():
             errs, rates = [], []
             for m in ladder:
@@ -79,7 +83,8 @@ def main():
                 errs.append(float(max(np.max(np.abs(o[c] - ref[c])) for c in range(2))))
                 rates.append(rate)
             slope = float(-np.polyfit(np.log(ladder), np.log(errs), 1)[0])
-            res[scheme] = {"steps": ladder, "errors": errs, "slope": round(slope, 3),
+            res[scheme] = {"steps": ladder, "errors": errs, "relative_errors": [e / refmax for e in errs],
+                           "slope": round(slope, 3),
                            "steps_per_s": [round(r, 1) for r in rates]}
         out[name] = res
         print(json.dumps({name: {k: (v.get("slope") if isinstance(v, dict) else None)
