@@ -548,3 +548,27 @@ def test_out_of_memory_is_reported(ctx, kx):
     ctx.tucker(X, Y, [dmat(np.eye(16)), dmat(np.eye(16))])
     ctx.sync()
     assert torch.equal(X, Y)
+
+
+def test_degenerate_and_invalid_grids(ctx, kx):
+    """Empty / oversized / unsupported grids are rejected synchronously; K = 0 (A_mu = 0) turns
+    exprk3ds into a pointwise ODE solver (phi_l(0) = I/l! exactly), matching the oracle; a tiny
+    tau gives phi-matrices equal to I/l! to rounding."""
+    for bad in ([0, 4], [4, 0, 3], [1 << 16, 1 << 16]):
+        with pytest.raises(kx.KxError):
+            ctx.set_grid(bad, 2)
+    with pytest.raises(kx.KxError):
+        ctx.set_grid([2] * 7, 2)
+    # K = 0
+    n = [12, 10]
+    prob = inputs.make_problem("fhn", 2, n, seed=4, amplitude=0.5)
+    prob.A = [[np.zeros((m, m)) for m in n] for _ in range(2)]
+    setup_problem(ctx, prob, "etd3rkds", 0.01)
+    out = run_gpu(ctx, prob, "etd3rkds", 0.01, 5)
+    ref, _ = integrate(prob, "etd3rkds", T=0.1, m=10, steps=5)
+    assert max(relerr(out[c], ref[c]) for c in range(2)) <= 1e-13
+    # tiny tau
+    prob = inputs.make_problem("schnakenberg", 2, 16)
+    setup_problem(ctx, prob, "etd3rkds", 1e-14)
+    P = ctx.phi_matrix(0, 2, 2, 1, 1)        # phi_2-term (l_2 = 2) at c = 1
+    assert np.max(np.abs(P - np.eye(16) / 2)) <= 1e-9
