@@ -89,7 +89,30 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if force or jobs or _newer(OUT, objs):
         cmd = [nvcc()] + ARCH + ["-shared", "-o", OUT] + objs + ["-cudart", "static", "-ldl"]
         run(cmd)
+    build_examples()
     return OUT
+
+
+def build_examples() -> None:
+    """C clients of the ABI (examples/*.c) -> build/<name>, linked against libkx.so."""
+    ex_dir = os.path.join(ROOT, "examples")
+    cc = shutil.which("gcc")
+    if not cc or not os.path.isdir(ex_dir):
+        return
+    cuda = os.path.dirname(os.path.dirname(nvcc()))
+    for f in sorted(os.listdir(ex_dir)):
+        if not f.endswith(".c"):
+            continue
+        src = os.path.join(ex_dir, f)
+        exe = os.path.join(ROOT, "build", f[:-2])
+        if not _newer(exe, [src, OUT, os.path.join(INCLUDE, "kx.h")]):
+            continue
+        cmd = [cc, "-O2", "-o", exe, src, "-I", INCLUDE, "-I", os.path.join(cuda, "include"),
+               "-L", PKG, "-lkx", "-L", os.path.join(cuda, "lib64"), "-lcudart",
+               "-Wl,-rpath," + PKG]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed: {' '.join(cmd)}\n{r.stderr}")
 
 
 if __name__ == "__main__":

@@ -152,3 +152,18 @@ def test_c4_size_linear_closed_form(kx, scheme):
     got = U[0].cpu().numpy()
     assert np.max(np.abs(got - expect)) / np.max(np.abs(expect)) <= 1e-11
     ctx.close()
+
+
+def test_c_client_example(kx):
+    """examples/schnakenberg_2d.c drives the library through the C ABI alone (no Python in the
+    loop) and reaches the Turing pattern's range at T = 2 (colour bar 0.6-1.8)."""
+    import os
+    import re
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "schnakenberg_2d")
+    assert os.path.exists(exe)
+    r = subprocess.run([exe, "64", "2000", "2"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lo, hi = map(float, re.findall(r"u in \[([0-9.]+), ([0-9.]+)\]", r.stdout)[-1])
+    assert 0.55 < lo < 0.8 and 1.5 < hi < 1.85, r.stdout
+    assert "40000 Tucker operators" in r.stdout    # 2000 steps x 2 species x 10 (P:671-673)
