@@ -161,8 +161,13 @@ kx_status kx_step_group(kx_ctx *const *ctxs, int nranks, double t, double *const
 /* ---------------------------------------------------------------- utilities -------- */
 kx_status kx_get_counters(const kx_ctx *ctx, kx_counters *out);
 kx_status kx_reset_counters(kx_ctx *ctx);
-/* Synchronise the context stream; returns KX_ERR_CUDA with a message on async failure. */
+/* Synchronise the context stream; returns KX_ERR_CUDA with a message on async failure, and
+ * KX_ERR_NUMERIC if the NaN watchdog (kx_set_nan_check) has fired. */
 kx_status kx_sync(kx_ctx *ctx);
+/* Per-step NaN/Inf watchdog (off by default): when on, every kx_step / kx_step_group also checks
+ * the updated U on the device; kx_sync then returns KX_ERR_NUMERIC naming the first step (counted
+ * from this call) whose result was non-finite.  Resets the step count and the flag. */
+kx_status kx_set_nan_check(kx_ctx *ctx, int on);
 /* KX_ERR_NUMERIC if any entry of the device tensor X (N doubles) is NaN/Inf (synchronous). */
 kx_status kx_check_finite(kx_ctx *ctx, const double *X);
 /* Per-launch CUDA-event timing of kx_step's kernels (disables graph replay while on).

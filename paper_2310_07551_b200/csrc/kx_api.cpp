@@ -80,6 +80,7 @@ void kx_destroy(kx_ctx* c) {
   for (auto e : c->ev_term)
     if (e) cudaEventDestroy(e);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->watch) cudaFree(c->watch);
   if (c->sk_ws) cudaFree(c->sk_ws);
   if (c->sk_flags) cudaFree(c->sk_flags);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -413,6 +414,23 @@ kx_status kx_sync(kx_ctx* c) {
   if (!c) return KX_ERR_INVALID;
   KX_CUDA(c, cudaStreamSynchronize(c->stream));
   KX_CUDA(c, cudaGetLastError());
+  if (c->nan_check && c->watch) {
+    int mon[2];
+    KX_CUDA(c, cudaMemcpy(mon, c->watch, sizeof(mon), cudaMemcpyDeviceToHost));
+    if (mon[1] >= 0)
+      return fail(c, KX_ERR_NUMERIC, "non-finite state after step " + std::to_string(mon[1] + 1) +
+                                         " (counting since kx_set_nan_check)");
+  }
+  return KX_OK;
+}
+
+kx_status kx_set_nan_check(kx_ctx* c, int on) {
+  if (!c) return KX_ERR_INVALID;
+  if (!c->watch) KX_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->watch), 2 * sizeof(int)));
+  const int init[2] = {0, -1};
+  KX_CUDA(c, cudaMemcpy(c->watch, init, sizeof(init), cudaMemcpyHostToDevice));
+  if ((c->nan_check != 0) != (on != 0)) drop_graph(c);
+  c->nan_check = on != 0;
   return KX_OK;
 }
 
@@ -589,7 +607,10 @@ kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const
                                            xr.count * 8, cudaMemcpyDeviceToDevice, ctxs[r]->stream));
     }
   }
-  for (int r = 0; r < nranks; ++r) ctxs[r]->cnt.steps += 1;
+  for (int r = 0; r < nranks; ++r) {
+    KX_TRY(enqueue_watch(ctxs[r], U + (size_t)r * nc));
+    ctxs[r]->cnt.steps += 1;
+  }
   return KX_OK;
 }
 

@@ -158,6 +158,9 @@ struct kx_ctx {
   double* halo_hi[MAXS] = {};
   double* F_pack[MAXS] = {};
 
+  int nan_check = 0;             // per-step NaN/Inf watchdog inside the step graph
+  int* watch = nullptr;          // device {steps completed, first bad step or -1}
+
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   struct Rec { int cls; int e0, e1; double flops; };
@@ -236,6 +239,7 @@ kx_status run_other(kx_ctx* c, F&& launch) {
 kx_status enqueue_step_etd3(kx_ctx* c, double* const* U);
 kx_status enqueue_step_etd2(kx_ctx* c, double* const* U);
 kx_status enqueue_step(kx_ctx* c, double* const* U);
+kx_status enqueue_watch(kx_ctx* c, double* const* U);
 kx_status step_impl(kx_ctx* c, double* const* U);
 // ---- kx_bank.cpp: phi-bank formation
 kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme);

@@ -349,6 +349,7 @@ kx_status dist_step_nccl(kx_ctx* c, double* const* U) {
     KX_TRY(dist_phase(c, U, ph, x));
     if (x.nbuf) KX_TRY(nccl_exchange(c, x, c->cur));
   }
+  KX_TRY(enqueue_watch(c, U));
   c->cnt.steps += 1;
   return KX_OK;
 }

@@ -101,6 +101,10 @@ cudaError_t launch_copy2d(double* Y, long long ldy, long long sy, const double* 
 cudaError_t launch_set_identity(double* Y, long long n, int nbatch, double v, cudaStream_t s);
 // flag[0] |= any(!isfinite(X[0..n)))
 cudaError_t launch_check_finite(const double* X, long long n, int* flag, cudaStream_t s);
+// watchdog: mon[1] = mon[0] (steps completed) if X holds a non-finite value and mon[1] == -1;
+// tick: mon[0] += 1
+cudaError_t launch_watch_finite(const double* X, long long n, int* mon, cudaStream_t s);
+cudaError_t launch_watch_tick(int* mon, cudaStream_t s);
 
 // Split coefficient tables (host).  Returns number of terms (0 if unsupported).
 int scheme_terms(int scheme, int ell, int d, double* eta, int* inner, double* alpha);

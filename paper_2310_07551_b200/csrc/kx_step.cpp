@@ -46,9 +46,17 @@ kx_status enqueue_step_etd2(kx_ctx* c, double* const* U) {
   return KX_OK;
 }
 
+kx_status enqueue_watch(kx_ctx* c, double* const* U) {
+  if (!c->nan_check) return KX_OK;
+  for (int s = 0; s < c->ncomp; ++s)
+    KX_TRY(run_other(c, [&] { return kx::launch_watch_finite(U[s], c->tN, c->watch, c->cur); }));
+  return run_other(c, [&] { return kx::launch_watch_tick(c->watch, c->cur); });
+}
+
 kx_status enqueue_step(kx_ctx* c, double* const* U) {
-  if (c->scheme == KX_ETD3RKDS_REAL || c->scheme == KX_ETD3RKDS_CPLX) return enqueue_step_etd3(c, U);
-  return enqueue_step_etd2(c, U);
+  if (c->scheme == KX_ETD3RKDS_REAL || c->scheme == KX_ETD3RKDS_CPLX) KX_TRY(enqueue_step_etd3(c, U));
+  else KX_TRY(enqueue_step_etd2(c, U));
+  return enqueue_watch(c, U);
 }
 
 kx_status step_impl(kx_ctx* c, double* const* U) {

@@ -194,6 +194,16 @@ __global__ void __launch_bounds__(256) kronsum_tridiag_kernel(const StencilArgs 
   }
 }
 
+// NaN/Inf watchdog (SURVEY §5 failure detection): mon = {steps completed, first bad step (-1)}
+__global__ void watch_finite_kernel(const double* __restrict__ x, long long n, int* mon) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicCAS(mon + 1, -1, mon[0]);
+}
+__global__ void watch_tick_kernel(int* mon) { mon[0] += 1; }
+
 int grid_for(long long work, int block) {
   static int nsm = 0;
   if (nsm == 0) {
@@ -265,6 +275,17 @@ cudaError_t launch_set_identity(double* Y, long long n, int nbatch, double v, cu
   if (n <= 0 || nbatch <= 0) return cudaSuccess;
   dim3 grid(grid_for(n * n, 256), nbatch);
   set_identity_kernel<<<grid, 256, 0, s>>>(Y, n, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_watch_finite(const double* X, long long n, int* mon, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  watch_finite_kernel<<<grid_for(n, 256), 256, 0, s>>>(X, n, mon);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_watch_tick(int* mon, cudaStream_t s) {
+  watch_tick_kernel<<<1, 1, 0, s>>>(mon);
   return cudaGetLastError();
 }
 

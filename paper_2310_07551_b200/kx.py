@@ -71,6 +71,7 @@ _SIGS = {
     "kx_reset_counters": (_i, [_vp]),
     "kx_sync": (_i, [_vp]),
     "kx_check_finite": (_i, [_vp, _vp]),
+    "kx_set_nan_check": (_i, [_vp, _i]),
     "kx_set_profiling": (_i, [_vp, _i]),
     "kx_get_profile": (_i, [_vp, _dp, _dp, C.POINTER(_ll), C.POINTER(_ll), _dp]),
     "kx_get_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
@@ -242,6 +243,9 @@ class Context:
 
     def sync(self):
         self._check(kx_sync(self.h))
+
+    def set_nan_check(self, on: bool):
+        self._check(kx_set_nan_check(self.h, 1 if on else 0))
 
     def check_finite(self, X) -> bool:
         st = kx_check_finite(self.h, _ptr(X))

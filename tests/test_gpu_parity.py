@@ -572,3 +572,26 @@ def test_degenerate_and_invalid_grids(ctx, kx):
     setup_problem(ctx, prob, "etd3rkds", 1e-14)
     P = ctx.phi_matrix(0, 2, 2, 1, 1)        # phi_2-term (l_2 = 2) at c = 1
     assert np.max(np.abs(P - np.eye(16) / 2)) <= 1e-9
+
+
+def test_nan_watchdog(ctx, kx):
+    """kx_set_nan_check: a blow-up (tau far beyond the stable range of an explicit-like
+    reaction, rho = 1e8) is reported by kx_sync as KX_ERR_NUMERIC with the step index."""
+    prob = inputs.make_problem("fhn", 2, [16, 16], seed=1, amplitude=1.0)
+    prob.params = dict(prob.params, rho=1e8)
+    setup_problem(ctx, prob, "etd3rkds", 0.5)
+    ctx.set_nan_check(True)
+    U = [dev(u) for u in prob.U0]
+    with pytest.raises(kx.KxError) as ei:
+        for _ in range(20):
+            ctx.step(U)
+        ctx.sync()
+    assert ei.value.status == kx.KX_ERR_NUMERIC and "step" in str(ei.value)
+    # a healthy run stays silent
+    prob = inputs.make_problem("fhn", 2, [16, 16], seed=1)
+    setup_problem(ctx, prob, "etd3rkds", 0.01)
+    ctx.set_nan_check(True)
+    U = [dev(u) for u in prob.U0]
+    for _ in range(5):
+        ctx.step(U)
+    ctx.sync()
