@@ -192,11 +192,17 @@ class OracleRunner:
                 f"excluded (random dense P of the same shapes)")
 
 
-def oracle_sample(cfg_name, seconds):
-    """(steps_per_s, cores, sample description) of a bounded oracle sample."""
+def oracle_sample(cfg_name, seconds, threads=None):
+    """(steps_per_s, cores, sample description) of a bounded oracle sample; `threads` limits
+    the BLAS thread pool (all host cores and one core)."""
     r = OracleRunner(cfg_name)
-    v, k = r.sample(seconds)
-    return v, r.cores(), r.describe(k)
+    if threads is None:
+        v, k = r.sample(seconds)
+        return v, r.cores(), r.describe(k)
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        v, k = r.sample(seconds)
+    return v, threads, r.describe(k).replace(f"on {os.cpu_count()} host cores", f"on {threads} core(s)")
 
 
 # -------------------------------------------------------------------------------- GPU arm --
@@ -276,40 +282,53 @@ def other_configs(kx, torch, stream, steps=10):
     return out
 
 
-def tucker_sweep(kx, torch, stream, budget_s=25.0):
-    """Tucker microbenchmark at a few sizes: dense flops / event time."""
+def tucker_sweep(kx, torch, stream, budget_s=40.0):
+    """Tucker microbenchmark: one Tucker operator T(X, {L_mu}) on an n^d
+    fp64 tensor, dense flops 2 N d n / device time.  R back-to-back Tuckers are captured in a
+    CUDA graph and replayed between CUDA events (no host launch overhead in the number); the
+    tensors of the larger sizes exceed L2, the small ones are L2-resident by nature."""
+    import inputs  # noqa: F401
     out = {}
     t_start = time.perf_counter()
-    for d, n in [(2, 1024), (3, 256), (3, 512), (2, 4096)]:
+    sizes = [(2, n) for n in (64, 128, 256, 512, 1024, 2048, 4096)] + \
+            [(3, n) for n in (64, 128, 256, 512, 1024)]
+    for d, n in sizes:
         if time.perf_counter() - t_start > budget_s:
             break
-        import inputs
         N = n ** d
+        fl = 2.0 * N * n * d
+        reps = int(min(200, max(3, 2e10 / fl)))
         ctx = kx.Context(stream.device.index, stream)
         ctx.set_grid([n] * d, 1)
-        A = inputs.laplacian_neumann(n, np.pi, 42.1887)
         X = torch.rand(N, dtype=torch.float64, device="cuda")
         Y = torch.empty_like(X)
         L = torch.rand(n * n, dtype=torch.float64, device="cuda") / n
         Ls = [L] * d
-        reps = 3 if N * n * d > 1e11 else 10
         for _ in range(2):
             ctx.tucker(X, Y, Ls)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record()
+        ctx.sync()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
             for _ in range(reps):
                 ctx.tucker(X, Y, Ls)
-            e1.record()
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        fl = 2.0 * N * n * d
-        out[f"d{d}_n{n}"] = round(fl / ms / 1e9, 2)
+        g.replay()
+        stream.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        best = None
+        for _ in range(3):
+            with torch.cuda.stream(stream):
+                e0.record()
+                g.replay()
+                e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            best = ms if best is None else min(best, ms)
+        out[f"d{d}_n{n}"] = round(fl / best / 1e9, 2)
+        del g
         ctx.close()
         del X, Y, L
         torch.cuda.empty_cache()
-        del A
     return out
 
 
@@ -539,6 +558,9 @@ def main():
         v, cores, sample = oracle_sample(args.config, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",
                                 "sample": sample}
+        v1, _, sample1 = oracle_sample(args.config, args.cpu_seconds / 2, threads=1)
+        line["cpu_baseline_1core"] = {"value": v1, "unit": "steps/s", "cores": 1, "kind": "oracle",
+                                      "sample": sample1}
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

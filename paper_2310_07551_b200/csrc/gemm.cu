@@ -101,10 +101,13 @@ struct Cfg {
 // the stream-K region (tiles [dp_tiles, T) with their k-iterations split into G_sk contiguous
 // ranges).  The cp.async producer runs STAGES-1 k-tiles ahead of the DMMA consumer ACROSS
 // tile boundaries, so the next tile's first stages load while this tile's epilogue runs.
-// Stream-K fix-up: a CTA whose range starts inside a tile stores its partial accumulators to
-// its workspace slot and raises its flag; the CTA owning the tile's first k-range adds the
-// later partials in increasing-k order (deterministic) and runs the epilogue.  Waits only go
-// to higher CTA indices, whose contribution is the first item of their stream-K range.
+// Stream-K fix-up: every CTA holding a k-range of a split tile stores its partial accumulators
+// to a workspace slot and counts itself in on the tile's counter; the contributors for which
+// the tile is the last item of their work list wait until all are in, then each sums a share
+// of the tile's fragments over the partials in increasing-k order (deterministic, independent
+// of which CTA sums) and stores it.  Waits happen only at the end of a CTA's list and only on
+// partials that are the first or last item of another CTA's list, so every wait ends (all
+// CTAs are co-resident: cooperative launch).
 struct Sched {
   int tiles_m = 1, tiles_n = 1, m_fastest = 0, ktiles = 0;
   int G = 1, G_sk = 0;
@@ -150,6 +153,18 @@ struct WorkIter {
     return false;
   }
 };
+
+// first stream-K unit of CTA i (i = G_sk: the end)
+__device__ __forceinline__ long long sk_begin(const Sched& sc, int i) {
+  return (long long)i * sc.sk_units / sc.G_sk;
+}
+// workspace slot of CTA i's partial of the split tile starting at unit t0u: a CTA holds at
+// most two split segments (the tail of the tile its range starts in, the head of the tile it
+// ends in), so slot 2i serves the first and 2i+1 the second and neither is overwritten while
+// the other tile's contributors may still read it
+__device__ __forceinline__ int sk_slot(const Sched& sc, int i, long long t0u) {
+  return 2 * i + (sk_begin(sc, i) >= t0u ? 0 : 1);
+}
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
 struct GemmTile {
@@ -263,7 +278,7 @@ struct GemmTile {
 
   // C = alpha*acc + beta*D + gamma*E + diag*[m==n]
   __device__ __forceinline__ static void epilogue(const GemmArgs& p, const Coord& cd,
-                                                  const double (&acc)[FM][FN][2]) {
+                                                  const double (&acc)[FM][FN][2], unsigned mask) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     const int wm0 = (warp / C_::WARPS_N) * WM, wn0 = (warp % C_::WARPS_N) * WN;
@@ -279,7 +294,7 @@ struct GemmTile {
 #pragma unroll
       for (int j = 0; j < FN; ++j) {
         const int n = cd.n0 + wn0 + j * 8 + 2 * t4;
-        if (n >= N) continue;
+        if (n >= N || !((mask >> (i * FN + j)) & 1u)) continue;
         double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
         if constexpr (VEC == 2) {
           if (D) {
@@ -393,7 +408,6 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   Coord cd = T_::coords(p, sc, cs.tl);
   double acc[FM][FN][2];
   T_::zero(acc);
-  double* ws_me = p.sk_ws + (size_t)cta * (FM * FN * 2 * NT);
   // the prefetch of k-tile t+STAGES-1 is issued behind the DMMAs of this tile's last k-step:
   // its empty-wait then targets a stage every warp left a whole k-tile ago (measured best of
   // k-step 0 / 4 / 12 / 28: +0.7% at C2)
@@ -424,32 +438,44 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     if (++ck < cs.ke) continue;
 
     // ---- segment finished
-    if (cs.kb > 0) {
-      // stream-K contributor: publish the partial (thread-fragment order, coalesced), signal
-#pragma unroll
-      for (int a = 0; a < FM; ++a)
-#pragma unroll
-        for (int c = 0; c < FN; ++c)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) __stcg(ws_me + ((a * FN + c) * 2 + e) * NT + tid, acc[a][c][e]);
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) atomicExch(p.sk_flags + cta, 1);
+    if (cs.kb == 0 && cs.ke == sc.ktiles) {
+      T_::epilogue(p, cd, acc, ~0u);
     } else {
-      if (cs.ke < sc.ktiles) {
-        // owner of a split tile: add the later k-ranges' partials in increasing k
-        const long long tr = cs.tl - sc.dp_tiles;
-        for (int j = cta + 1; j < sc.G_sk; ++j) {
-          const long long bj = (long long)j * sc.sk_units / sc.G_sk;
-          if (bj >= (tr + 1) * sc.ktiles) break;
-          if (tid == 0) {
-            volatile int* f = p.sk_flags + j;
-            while (*f == 0) __nanosleep(64);
-            __threadfence();
-            *f = 0;
-          }
-          __syncthreads();
-          const double* wj = p.sk_ws + (size_t)j * (FM * FN * 2 * NT);
+      // split tile (stream-K): every contributor publishes its partial and counts itself in.
+      // The contributors whose work list ENDS in this tile (all but a tail CTA that continues
+      // into the next tile) then wait for the rest and each sums a 1/nr share of the
+      // fragments over all partials in increasing-k order (contributor order: the result does
+      // not depend on who sums) and stores it.  Only a CTA's last segment ever waits, so no
+      // CTA's own work queues behind a wait.
+      const long long tr = cs.tl - sc.dp_tiles;
+      const long long t0u = tr * sc.ktiles, t1u = t0u + sc.ktiles;
+      int i0 = cta, i1 = cta;
+      while (i0 > 0 && sk_begin(sc, i0) > t0u) --i0;
+      while (i1 + 1 < sc.G_sk && sk_begin(sc, i1 + 1) < t1u) ++i1;
+      const int nc = i1 - i0 + 1;
+      const int nr = sk_begin(sc, i1 + 1) <= t1u ? nc : nc - 1;   // reducers: i0 .. i0+nr-1
+      int* arrive = p.sk_flags + 2 * tr;
+      const int q = cta - i0;
+      const bool solo = nr == 1 && q == 0;   // the only reducer keeps its own partial in registers
+      if (!solo) {
+        double* ws_me = p.sk_ws + (size_t)sk_slot(sc, cta, t0u) * (FM * FN * 2 * NT);
+#pragma unroll
+        for (int a = 0; a < FM; ++a)
+#pragma unroll
+          for (int c = 0; c < FN; ++c)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) __stcg(ws_me + ((a * FN + c) * 2 + e) * NT + tid, acc[a][c][e]);
+        __threadfence();
+        __syncthreads();
+      }
+      if (solo) {
+        if (tid == 0) {
+          while (*reinterpret_cast<volatile int*>(arrive) < nc - 1) __nanosleep(32);
+          __threadfence();
+        }
+        __syncthreads();
+        for (int j = i0 + 1; j <= i1; ++j) {
+          const double* wj = p.sk_ws + (size_t)sk_slot(sc, j, t0u) * (FM * FN * 2 * NT);
 #pragma unroll
           for (int a = 0; a < FM; ++a)
 #pragma unroll
@@ -457,8 +483,41 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
 #pragma unroll
               for (int e = 0; e < 2; ++e) acc[a][c][e] += __ldcg(wj + ((a * FN + c) * 2 + e) * NT + tid);
         }
+        T_::epilogue(p, cd, acc, ~0u);
+        if (tid == 0) arrive[0] = 0;
+      } else if (q < nr) {
+        if (tid == 0) {
+          atomicAdd(arrive, 1);
+          while (*reinterpret_cast<volatile int*>(arrive) < nc) __nanosleep(32);
+          __threadfence();
+        }
+        __syncthreads();
+        unsigned mask = 0;
+#pragma unroll
+        for (int f = 0; f < FM * FN; ++f)
+          if (f % nr == q) mask |= 1u << f;
+        T_::zero(acc);
+        for (int j = i0; j <= i1; ++j) {
+          const double* wj = p.sk_ws + (size_t)sk_slot(sc, j, t0u) * (FM * FN * 2 * NT);
+#pragma unroll
+          for (int a = 0; a < FM; ++a)
+#pragma unroll
+            for (int c = 0; c < FN; ++c)
+              if ((mask >> (a * FN + c)) & 1u) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) acc[a][c][e] += __ldcg(wj + ((a * FN + c) * 2 + e) * NT + tid);
+              }
+        }
+        T_::epilogue(p, cd, acc, mask);
+        __syncthreads();
+        if (tid == 0 && atomicAdd(arrive + 1, 1) == nr - 1) {   // last reducer out resets
+          arrive[0] = 0;
+          arrive[1] = 0;
+          __threadfence();
+        }
+      } else if (tid == 0) {
+        atomicAdd(arrive, 1);   // a tail contributor that continues into the next tile
       }
-      T_::epilogue(p, cd, acc);
     }
     if (!cit.next(cs)) break;
     ck = cs.kb;
@@ -515,19 +574,34 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
   const long long Gmax = (long long)num_sms() * P_::occ;
   sc.G = (int)std::min<long long>(T, Gmax);
   sc.dp_tiles = T;
-  const bool sk_ok = g.sk_ws && g.sk_flags && Gmax <= kSkSlots * (128 * 128) / (BM * BN) &&
-                     Gmax <= kSkFlags && sc.ktiles >= 8;
+  // stream-K needs two workspace slots per CTA and a counter pair per split tile
+  const bool sk_ok = g.sk_ws && g.sk_flags && 2 * Gmax * BM * BN <= (long long)kSkSlots * 128 * 128 &&
+                     sc.ktiles >= 2;
   if (sk_ok && T % Gmax != 0) {
-    const double waves = (double)T / Gmax;
-    if (std::ceil(waves) / waves > 1.06) {   // classic tail would waste > 6%
-      long long dp = (T / Gmax) * Gmax;
-      if (dp >= Gmax && (T - dp) * 2 < Gmax) dp -= Gmax;   // short tail: spread one more wave
-      sc.G = (int)Gmax;
+    long long dp = (T / Gmax) * Gmax;
+    if (dp >= Gmax && (T - dp) * 2 < Gmax) dp -= Gmax;   // short tail: spread one more wave
+    // >= 4 k-tiles per CTA behind a data-parallel part, >= 2 when the whole launch is split
+    const long long units = (T - dp) * sc.ktiles;
+    const int G_sk = (int)std::min<long long>(Gmax, units / (dp > 0 ? 4 : 2));
+    // time model in k-tile units: the split costs its fix-up (~3 us: partial store, fence,
+    // counter, partial loads) on top of the longest k-range
+    const double kt_us = 4.2 * (BM * BN * BK) / (128.0 * 128 * 32) * P_::occ;
+    const double classic = std::ceil((double)T / Gmax) * sc.ktiles;
+    const double split = (double)(dp / Gmax) * sc.ktiles +
+                         std::ceil((double)units / std::max(G_sk, 1)) + 3.0 / kt_us;
+    const bool worth = dp > 0 || (long long)g.kseg * g.nseg >= 128;   // tiny K: latency-bound
+    if (worth && G_sk >= 1 && 2 * (T - dp) <= kSkFlags && split < 0.97 * classic) {
+      sc.G = dp > 0 ? (int)Gmax : G_sk;
       sc.dp_tiles = dp;
-      sc.sk_units = (T - dp) * sc.ktiles;
-      sc.G_sk = (int)std::min<long long>(Gmax, sc.sk_units / 4);
+      sc.sk_units = units;
+      sc.G_sk = G_sk;
     }
   }
+  static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only
+  if (trace)
+    fprintf(stderr, "kx-gemm %s M=%d N=%d K=%dx%d nz=%d cfg=%dx%dx%d tiles=%lld kt=%d G=%d dp=%lld sk_units=%lld G_sk=%d flops=%.4g\n",
+            AROW ? "row" : "col", g.M, g.N, g.kseg, g.nseg, nz, BM, BN, BK, T, sc.ktiles, sc.G,
+            sc.dp_tiles, sc.sk_units, sc.G_sk, 2.0 * g.M * g.N * (double)g.kseg * g.nseg * nz);
   if (sc.sk_units > 0) {
     // stream-K CTAs wait on each other: a cooperative launch guarantees that the whole grid is
     // co-resident even when other kernels share the GPU (otherwise the driver refuses it)

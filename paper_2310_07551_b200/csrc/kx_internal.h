@@ -35,8 +35,8 @@ struct GemmArgs {
   double* sk_ws = nullptr;
   int* sk_flags = nullptr;
 };
-constexpr int kSkSlots = 160;    // partial-tile slots of 128x128 doubles (>= SM count)
-constexpr int kSkFlags = 1024;   // flags (>= resident CTAs of any config)
+constexpr int kSkSlots = 304;    // partial-tile slots of 128x128 doubles (>= 2 x SM count)
+constexpr int kSkFlags = 2048;   // counters: a pair per split tile
 
 // Launch on `stream`; returns cudaSuccess or the launch error.  Chooses tile config.
 cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);

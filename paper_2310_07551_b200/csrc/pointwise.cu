@@ -131,65 +131,80 @@ __global__ void check_finite_kernel(const double* __restrict__ x, long long n, i
 // threads along the contiguous i_1: every load is coalesced along i_1 and the i_mu +- 1
 // neighbours (mu >= 2) are other lines read by neighbouring CTAs, so each X element is fetched
 // from HBM about once.  HBM-bound: 8 B (X) + 8 B (Dd) + 8 B (Y) per point.
+template <int D, typename I>
+__device__ __forceinline__ double tridiag_point(const StencilArgs& a, int s, const double* __restrict__ X,
+                                                I p) {
+  // multi-index of point p (32-bit arithmetic when the tensor fits)
+  const I n1 = (I)a.n[0];
+  I rem = p / n1;
+  const I i1 = p - rem * n1;
+  I idx[D > 1 ? D : 2], str[D > 1 ? D : 2];
+  I stride = n1;
+#pragma unroll
+  for (int mu = 1; mu < D; ++mu) {
+    const I nm = (I)a.n[mu];
+    const I q = rem / nm;
+    idx[mu] = rem - q * nm;
+    rem = q;
+    str[mu] = stride;
+    stride *= nm;
+  }
+  const double xp = X[p];
+  double acc = a.Dd[s] ? a.beta * a.Dd[s][p] : 0.0;
+  // mu = d .. 2 (descending, as the dense path)
+#pragma unroll
+  for (int mu = D - 1; mu >= 1; --mu) {
+    const I i = idx[mu], st = str[mu];
+    const bool sh = (mu == D - 1) && a.n_glob_d != 0;
+    const long long ig = sh ? (long long)i + a.d_off : (long long)i;
+    const long long ng = sh ? a.n_glob_d : a.n[mu];
+    double t = a.di[s][mu][ig] * xp;
+    if (sh) {
+      // sharded last direction: neighbour planes from the halos
+      const I pp = p - i * st;   // offset inside the plane
+      if (ig > 0) t = fma(a.lo[s][mu][ig], i > 0 ? X[p - st] : a.halo_lo[s][pp], t);
+      if (ig + 1 < ng) t = fma(a.up[s][mu][ig], i + 1 < (I)a.n[mu] ? X[p + st] : a.halo_hi[s][pp], t);
+    } else {
+      if (i > 0) t = fma(a.lo[s][mu][i], X[p - st], t);
+      if (i + 1 < (I)ng) t = fma(a.up[s][mu][i], X[p + st], t);
+    }
+    acc += t;
+  }
+  double t = a.di[s][0][i1] * xp;
+  if (i1 > 0) t = fma(a.lo[s][0][i1], X[p - 1], t);
+  if (i1 + 1 < n1) t = fma(a.up[s][0][i1], X[p + 1], t);
+  return acc + t;
+}
+
+// Grid-stride over points, U points per thread in flight (their loads are independent, so
+// U x ~10 loads are outstanding per thread: the kernel is bound by bytes in flight).
+template <int D, typename I, int U>
 __global__ void __launch_bounds__(256) kronsum_tridiag_kernel(const StencilArgs a) {
   const int s = blockIdx.y;
   const double* __restrict__ X = a.X[s];
   double* __restrict__ Y = a.Y[s];
-  const double* __restrict__ Dd = a.Dd[s];
-  const long long n1 = a.n[0];
-  const long long lines = a.N / n1;
-  for (long long line = blockIdx.x; line < lines; line += gridDim.x) {
-    // multi-index of the line and the strides of each direction
-    long long rem = line, stride = n1;
-    long long idx[6], str[6];
-    idx[0] = 0;
-    str[0] = 1;
+  const I N = (I)a.N;
+  const I step = (I)gridDim.x * blockDim.x;
+  for (I p0 = (I)blockIdx.x * blockDim.x + threadIdx.x; p0 < N; p0 += U * step) {
+    double v[U];
 #pragma unroll
-    for (int mu = 1; mu < 6; ++mu) {
-      if (mu < a.d) {
-        idx[mu] = rem % a.n[mu];
-        rem /= a.n[mu];
-        str[mu] = stride;
-        stride *= a.n[mu];
-      }
+    for (int u = 0; u < U; ++u) {
+      const I p = p0 + u * step;
+      v[u] = p < N ? tridiag_point<D, I>(a, s, X, p) : 0.0;
     }
-    const long long base = line * n1;
-    for (long long i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
-      const long long p = base + i1;
-      double acc = Dd ? a.beta * Dd[p] : 0.0;
-      // mu = d .. 2 (descending, as the dense path)
 #pragma unroll
-      for (int mu = 5; mu >= 1; --mu) {
-        if (mu < a.d) {
-          const long long i = idx[mu], nm = a.n[mu], st = str[mu];
-          if (mu == a.d - 1 && a.n_glob_d) {
-            // sharded last direction: global index, neighbour planes from the halos
-            const long long ig = i + a.d_off;
-            const long long pp = p - i * st;   // offset inside the plane
-            double t = a.di[s][mu][ig] * X[p];
-            if (ig > 0) t = fma(a.lo[s][mu][ig], i > 0 ? X[p - st] : a.halo_lo[s][pp], t);
-            if (ig + 1 < a.n_glob_d) t = fma(a.up[s][mu][ig], i + 1 < nm ? X[p + st] : a.halo_hi[s][pp], t);
-            acc += t;
-          } else {
-            double t = a.di[s][mu][i] * X[p];
-            if (i > 0) t = fma(a.lo[s][mu][i], X[p - st], t);
-            if (i + 1 < nm) t = fma(a.up[s][mu][i], X[p + st], t);
-            acc += t;
-          }
+    for (int u = 0; u < U; ++u) {
+      const I p = p0 + u * step;
+      if (p < N) {
+        I o = p;
+        if (a.pack_n1l) {   // peer-packed output (distributed contexts)
+          const I n1 = (I)a.n[0], n1l = (I)a.pack_n1l;
+          const I line = p / n1, i1 = p - line * n1;
+          const I q = i1 / n1l;
+          o = q * (N / n1 * n1l) + line * n1l + (i1 - q * n1l);
         }
+        Y[o] = v[u];
       }
-      {
-        double t = a.di[s][0][i1] * X[p];
-        if (i1 > 0) t = fma(a.lo[s][0][i1], X[p - 1], t);
-        if (i1 + 1 < n1) t = fma(a.up[s][0][i1], X[p + 1], t);
-        acc += t;
-      }
-      long long o = p;
-      if (a.pack_n1l) {   // peer-packed output (distributed contexts)
-        const long long q = i1 / a.pack_n1l;
-        o = q * (a.N / n1 * a.pack_n1l) + line * a.pack_n1l + (i1 - q * a.pack_n1l);
-      }
-      Y[o] = acc;
     }
   }
 }
@@ -240,12 +255,28 @@ cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t s
 
 cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream) {
   if (a.N <= 0) return cudaSuccess;
-  const long long lines = a.N / a.n[0];
-  const int block = a.n[0] >= 256 ? 256 : (a.n[0] >= 128 ? 128 : 64);
-  long long g = lines;
-  const long long cap = 148LL * 16;
-  if (g > cap) g = cap;
-  kronsum_tridiag_kernel<<<dim3((unsigned)g, a.ns), block, 0, stream>>>(a);
+  // U = 4 points per thread in flight on large grids; small grids spread one point per
+  // thread over more CTAs (latency-bound there)
+  constexpr int block = 256;
+  const bool wide = a.N >= 148LL * block * 4 * 2;
+  const dim3 grid((unsigned)grid_for(wide ? (a.N + 3) / 4 : a.N, block), a.ns);
+  const bool small = a.N < (1LL << 30);   // 32-bit point indices (p + st stays < 2^31)
+#define KX_TRIDIAG(DD)                                                                    \
+  case DD:                                                                                \
+    if (!small) kronsum_tridiag_kernel<DD, long long, 4><<<grid, block, 0, stream>>>(a);  \
+    else if (wide) kronsum_tridiag_kernel<DD, int, 4><<<grid, block, 0, stream>>>(a);     \
+    else kronsum_tridiag_kernel<DD, int, 1><<<grid, block, 0, stream>>>(a);               \
+    break;
+  switch (a.d) {
+    KX_TRIDIAG(1)
+    KX_TRIDIAG(2)
+    KX_TRIDIAG(3)
+    KX_TRIDIAG(4)
+    KX_TRIDIAG(5)
+    KX_TRIDIAG(6)
+    default: return cudaErrorInvalidValue;
+  }
+#undef KX_TRIDIAG
   return cudaGetLastError();
 }
 
