@@ -131,9 +131,18 @@ kx_status kx_phi_apply(kx_ctx *ctx, int comp, int ell, int stage, const double *
  * (HOST array of device pointers).  t is the time at the start of the step (the built-in
  * models are autonomous).  Replays a cached CUDA graph when the U pointers repeat. */
 kx_status kx_step(kx_ctx *ctx, double t, double *const *U);
+/* nsteps (>= 0) consecutive kx_step calls from time t0.  On a small 2-D grid (see
+ * kx_set_fused_small) all nsteps run inside ONE kernel launch; otherwise the step graph is
+ * replayed nsteps times.  With the NaN watchdog on, steps are launched one by one. */
+kx_status kx_step_n(kx_ctx *ctx, double t0, int nsteps, double *const *U);
 /* Same as kx_step but U are HOST buffers (N doubles each): copies them to the device,
- * steps `nsteps` times, copies back, synchronises (end-to-end entry point). */
+ * steps `nsteps` times (as kx_step_n), copies back, synchronises (end-to-end entry point). */
 kx_status kx_integrate_host(kx_ctx *ctx, double t0, int nsteps, double *const *U_host);
+/* Small 2-D grids (d = 2, 8 <= n_2 <= 64, n_1 <= 64, tridiagonal A_mu, real scheme, one GPU):
+ * on = 1 (default) executes each step as ONE kernel on an 8-CTA thread-block cluster that
+ * keeps the state in shared memory and fuses the mode-2 and mode-1 products of every term
+ * (the shape of eq:exp2d; SURVEY §2 K*5); on = 0 forces the general path. */
+kx_status kx_set_fused_small(kx_ctx *ctx, int on);
 
 /* ---------------------------------------------------------------- multi-GPU -------- */
 /* Slab decomposition along i_d over P ranks (one process per GPU); see DESIGN.md §8.

@@ -373,6 +373,46 @@ kx_status kx_step(kx_ctx* c, double t, double* const* U) {
   return step_impl(c, U);
 }
 
+kx_status kx_set_fused_small(kx_ctx* c, int on) {
+  if (!c) return KX_ERR_INVALID;
+  if ((c->fused_small != 0) != (on != 0)) drop_graph(c);
+  c->fused_small = on != 0;
+  return KX_OK;
+}
+
+namespace {
+// nsteps steps on device tensors that passed kx_step's checks (one GPU)
+kx_status steps_impl(kx_ctx* c, double* const* U, int nsteps) {
+  if (nsteps > 0 && !c->nan_check && !c->profiling && fused_eligible(c)) {
+    c->cur = c->stream;
+    KX_TRY(enqueue_fused(c, U, nsteps));
+    c->cnt.steps += nsteps;
+    return KX_OK;
+  }
+  for (int k = 0; k < nsteps; ++k) KX_TRY(step_impl(c, U));
+  return KX_OK;
+}
+}  // namespace
+
+kx_status kx_step_n(kx_ctx* c, double t0, int nsteps, double* const* U) {
+  (void)t0;
+  KX_TRY(need_grid(c));
+  if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
+  if (!U || nsteps < 0) return fail(c, KX_ERR_INVALID, "bad arguments");
+  if (c->model != 0 && c->ncomp != 2) return fail(c, KX_ERR_INVALID, "model needs 2 components");
+  for (int s = 0; s < c->ncomp; ++s) {
+    KX_TRY(check_ptr(c, U[s], "U[c]"));
+    for (int r = 0; r < s; ++r)
+      if (U[r] == U[s]) return fail(c, KX_ERR_INVALID, "U components must be distinct");
+  }
+  if (c->dist == 2) return fail(c, KX_ERR_INVALID, "loopback group members step through kx_step_group");
+  if (c->dist == 1) {
+    for (int k = 0; k < nsteps; ++k) KX_TRY(dist_step_nccl(c, U));
+    return KX_OK;
+  }
+  return steps_impl(c, U, nsteps);
+}
+
 kx_status kx_integrate_host(kx_ctx* c, double t0, int nsteps, double* const* U_host) {
   KX_TRY(need_grid(c));
   if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
@@ -387,11 +427,8 @@ kx_status kx_integrate_host(kx_ctx* c, double t0, int nsteps, double* const* U_h
     }
     KX_CUDA(c, cudaMemcpyAsync(c->hostU[s], U_host[s], bytes, cudaMemcpyHostToDevice, c->stream));
   }
-  double t = t0;
-  for (int k = 0; k < nsteps; ++k) {
-    KX_TRY(step_impl(c, c->hostU));
-    t += c->tau;
-  }
+  (void)t0;
+  KX_TRY(steps_impl(c, c->hostU, nsteps));
   for (int s = 0; s < c->ncomp; ++s)
     KX_CUDA(c, cudaMemcpyAsync(U_host[s], c->hostU[s], bytes, cudaMemcpyDeviceToHost, c->stream));
   KX_CUDA(c, cudaStreamSynchronize(c->stream));

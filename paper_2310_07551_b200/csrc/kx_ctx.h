@@ -90,6 +90,7 @@ struct kx_ctx {
   std::vector<std::vector<double*>> A_dev;                 // [c][mu]
   std::vector<std::vector<double*>> A_tri;                 // [c][mu]: lo|di|up (3 n) or null
   int kronsum_mode = 0;   // 0 auto (tridiagonal stencil when every A is tridiagonal), 1 dense
+  int fused_small = 1;    // 1: small 2-D grids step in one cluster kernel (K*5, fused2d.cu)
 
   int model = 0;
   double params[8] = {};
@@ -240,6 +241,8 @@ kx_status enqueue_step_etd3(kx_ctx* c, double* const* U);
 kx_status enqueue_step_etd2(kx_ctx* c, double* const* U);
 kx_status enqueue_step(kx_ctx* c, double* const* U);
 kx_status enqueue_watch(kx_ctx* c, double* const* U);
+bool fused_eligible(const kx_ctx* c);
+kx_status enqueue_fused(kx_ctx* c, double* const* U, int nsteps);
 kx_status step_impl(kx_ctx* c, double* const* U);
 // ---- kx_bank.cpp: phi-bank formation
 kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme);

@@ -87,6 +87,26 @@ struct StencilArgs {
 };
 cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream);
 
+// Kernel K*5 (fused2d.cu): nsteps whole ETD2RKDS / exprk3ds_real steps of a small 2-D grid
+// (8 <= n2 <= kFusedNMax, n1 <= kFusedNMax, tridiagonal A_mu) in one 8-CTA cluster.
+constexpr int kFusedCluster = 8;
+constexpr int kFusedNMax = 64;
+constexpr int kFusedMaxSeg = 6;
+struct Fused2dArgs {
+  int n1 = 0, n2 = 0, ncomp = 2, model = 0, nsteps = 1, nstages = 2;
+  double p[8] = {};
+  double* U[2] = {};
+  const double* tri[2][2] = {};            // [species][mu-1]: lo | di | up (3 n_mu doubles)
+  int nseg[3] = {}, base[3] = {};          // base: 0 = U, 1 = the previous stage value
+  int seg_in[3][kFusedMaxSeg] = {};        // 0 = F, 1 = D
+  const double* P2[3][kFusedMaxSeg][2] = {};   // mode-2 matrix, column-major, leading dim ld2
+  long long ld2[3][kFusedMaxSeg] = {};
+  const double* B[3][kFusedMaxSeg][2] = {};    // scaled mode-1 block, row-major n1 x n1
+  long long* prof = nullptr;                   // diagnostics: clock64 phase stamps (<= 64)
+};
+cudaError_t launch_fused2d(const Fused2dArgs& a, cudaStream_t stream);
+size_t fused2d_smem_bytes();
+
 // Y = alpha * X (elementwise, n doubles); used for bank assembly.
 cudaError_t launch_scale(double* Y, const double* X, double alpha, long long n, cudaStream_t s);
 // Y = a X1 + b X2 (elementwise, n doubles); complex bank blocks.

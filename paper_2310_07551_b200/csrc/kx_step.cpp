@@ -1,6 +1,9 @@
 // One-GPU step schedules (ETD2RKDS, exprk3ds) and their CUDA-graph capture / replay.
 #include "kx_ctx.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace kx::detail {
 
 // ---------------------------------------------------------------- time steps --------------
@@ -53,8 +56,98 @@ kx_status enqueue_watch(kx_ctx* c, double* const* U) {
   return run_other(c, [&] { return kx::launch_watch_tick(c->watch, c->cur); });
 }
 
+// ---------------------------------------------------------------- small 2-D grids (K*5) ---
+// Eligible: one GPU, d = 2, real scheme, <= 2 species, 8 <= n_2 <= 64, n_1 <= 64, every A_mu
+// tridiagonal (the stencil form of the Kronecker sum).
+bool fused_eligible(const kx_ctx* c) {
+  if (!c->fused_small || c->dist || c->cplx || c->d != 2 || c->ncomp < 1 || c->ncomp > 2) return false;
+  if (c->scheme != KX_ETD2RKDS && c->scheme != KX_ETD3RKDS_REAL) return false;
+  const long long n1 = c->tn[0], n2 = c->tn[1];
+  if (n1 < 1 || n1 > kx::kFusedNMax || n2 < kx::kFusedCluster || n2 > kx::kFusedNMax) return false;
+  if (!all_tridiag(c, 0, c->ncomp)) return false;
+  for (int k = 0; k < c->nstages; ++k)
+    if (c->stages[k].nseg > kx::kFusedMaxSeg) return false;
+  return c->nstages == 2 || c->nstages == 3;
+}
+
+// nsteps steps of the current scheme in one cluster launch.  The stage banks are the ones the
+// general path uses: stage k's segment sg reads group gi's term t (first-mode matrix
+// group.first + t n_2, leading dimension nterms n_2) and the scaled mode-1 block
+// stage.B + sg n_1^2.
+kx_status enqueue_fused(kx_ctx* c, double* const* U, int nsteps) {
+  kx::Fused2dArgs a;
+  const long long n1 = c->tn[0], n2 = c->tn[1];
+  const bool etd3 = c->nstages == 3;
+  a.n1 = (int)n1;
+  a.n2 = (int)n2;
+  a.ncomp = c->ncomp;
+  a.model = c->model;
+  a.nsteps = nsteps;
+  a.nstages = c->nstages;
+  for (int i = 0; i < 8; ++i) a.p[i] = c->params[i];
+  for (int s = 0; s < c->ncomp; ++s) {
+    a.U[s] = U[s];
+    for (int mu = 0; mu < 2; ++mu) a.tri[s][mu] = c->A_tri[s][mu];
+  }
+  const Group& F = c->groups[0];
+  for (int k = 0; k < c->nstages; ++k) {
+    const Stage& st = c->stages[k];
+    a.nseg[k] = st.nseg;
+    a.base[k] = (!etd3 && k == 1) ? 1 : 0;
+    for (int sg = 0; sg < st.nseg; ++sg) {
+      const int slot = st.slot[sg];
+      const bool from_f = slot < F.slot0 + F.nterms;
+      const Group& G = from_f ? F : c->groups[etd3 ? k : 1];
+      const int t = slot - G.slot0;
+      a.seg_in[k][sg] = from_f ? 0 : 1;
+      a.ld2[k][sg] = (long long)G.nterms * n2;
+      for (int s = 0; s < c->ncomp; ++s) {
+        a.P2[k][sg][s] = G.first[s] + t * n2;
+        a.B[k][sg][s] = st.B[s] + (long long)sg * n1 * n1;
+      }
+    }
+  }
+  // algorithmic work of the steps, counted as on the general path
+  const long long tuckers = (long long)c->ncomp * (etd3 ? 5 * c->T : 2) * nsteps;
+  const double fl = 2.0 * (double)c->tN * (double)(n1 + n2) * (double)tuckers;
+  int e0 = -1;
+  if (c->profiling) {
+    e0 = c->ev_used;
+    c->ev_used += 2;
+    KX_CUDA(c, record(c, pool_event(c, e0)));
+  }
+  // diagnostics only: KX_FUSED_PROF=1 prints phase clocks of eager (not captured) launches
+  static long long* prof_buf = nullptr;
+  long long* prof = nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->cur, &cap);
+  if (getenv("KX_FUSED_PROF") && cap == cudaStreamCaptureStatusNone) {
+    if (!prof_buf && cudaMallocManaged(&prof_buf, 64 * sizeof(long long)) != cudaSuccess) prof_buf = nullptr;
+    prof = prof_buf;
+  }
+  a.prof = prof;
+  KX_CUDA(c, kx::launch_fused2d(a, c->cur));
+  if (prof) {
+    KX_CUDA(c, cudaStreamSynchronize(c->cur));
+    fprintf(stderr, "kx-fused phases (cycles):");
+    for (int i = 1; i < 64 && prof[i] > prof[i - 1]; ++i) fprintf(stderr, " %lld", prof[i] - prof[i - 1]);
+    fprintf(stderr, "\n");
+  }
+  if (c->profiling) {
+    KX_CUDA(c, record(c, pool_event(c, e0 + 1)));
+    c->recs.push_back({0, e0, e0 + 1, fl});
+  }
+  c->cnt.gemm_launches += 1;
+  c->cnt.tucker_ops += tuckers;
+  c->cnt.mode_products += 2 * tuckers + (long long)c->ncomp * 2 * nsteps;
+  c->cnt.kronsum_actions += (long long)c->ncomp * nsteps;
+  c->cnt.mode_product_flops += fl;
+  return KX_OK;
+}
+
 kx_status enqueue_step(kx_ctx* c, double* const* U) {
-  if (c->scheme == KX_ETD3RKDS_REAL || c->scheme == KX_ETD3RKDS_CPLX) KX_TRY(enqueue_step_etd3(c, U));
+  if (fused_eligible(c)) KX_TRY(enqueue_fused(c, U, 1));
+  else if (c->scheme == KX_ETD3RKDS_REAL || c->scheme == KX_ETD3RKDS_CPLX) KX_TRY(enqueue_step_etd3(c, U));
   else KX_TRY(enqueue_step_etd2(c, U));
   return enqueue_watch(c, U);
 }

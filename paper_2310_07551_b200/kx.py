@@ -62,6 +62,8 @@ _SIGS = {
     "kx_phi_apply": (_i, [_vp, _i, _i, _i, _vp, _vp, _d, _d]),
     "kx_step": (_i, [_vp, _d, C.POINTER(_vp)]),
     "kx_integrate_host": (_i, [_vp, _d, _i, C.POINTER(_vp)]),
+    "kx_step_n": (_i, [_vp, _d, _i, C.POINTER(_vp)]),
+    "kx_set_fused_small": (_i, [_vp, _i]),
     "kx_nccl_unique_id": (_i, [_vp]),
     "kx_create_dist": (_i, [C.POINTER(_vp), _i, _vp, _vp, _i, _i]),
     "kx_create_group": (_i, [C.POINTER(_vp), _i, _i, _vp]),
@@ -227,6 +229,13 @@ class Context:
     def step(self, U: list, t: float = 0.0):
         arr = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
         self._check(kx_step(self.h, t, arr))
+
+    def step_n(self, U: list, nsteps: int, t0: float = 0.0):
+        arr = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
+        self._check(kx_step_n(self.h, t0, nsteps, arr))
+
+    def set_fused_small(self, on: bool):
+        self._check(kx_set_fused_small(self.h, 1 if on else 0))
 
     def integrate_host(self, U_host: list[np.ndarray], nsteps: int, t0: float = 0.0):
         """U_host: C-contiguous float64 host arrays (pinned torch tensors work too: pass

@@ -595,3 +595,80 @@ def test_nan_watchdog(ctx, kx):
     for _ in range(5):
         ctx.step(U)
     ctx.sync()
+
+
+# ---------------------------------------------------------------- K*5: fused small 2-D grids
+@pytest.mark.parametrize("case", [("schnakenberg", [64, 64], "etd2rkds", 1.0 / 3000, 1.0),
+                                  ("schnakenberg", [64, 64], "etd3rkds", 1.0 / 3000, 1.0),
+                                  ("fhn", [48, 40], "etd3rkds", 0.01, 1.0),
+                                  ("fhn", [33, 20], "etd2rkds", 0.01, 1.0),
+                                  ("schnakenberg", [7, 8], "etd3rkds", 1e-5, 1.0),
+                                  ("schnakenberg", [64, 9], "etd2rkds", 1e-5, 1.0)])
+def test_fused_small_vs_general_and_oracle(kx, case):
+    """The one-cluster step kernel (kx_set_fused_small, default on) against the general
+    multi-launch path and against the oracle: 3 steps, element by element."""
+    from oracle import etd
+    model, n, scheme, tau, amp = case
+    prob = inputs.make_problem(model, 2, n, seed=11, amplitude=amp)
+    out = {}
+    for fused in (True, False):
+        c = kx.Context(0)
+        setup_problem(c, prob, scheme, tau)
+        c.set_fused_small(fused)
+        U = [dev(u) for u in prob.U0]
+        c.reset_counters()
+        for _ in range(3):
+            c.step(U)
+        c.sync()
+        out[fused] = [u.cpu().numpy() for u in U]
+        cnt = c.counters()
+        per = 10 if scheme == "etd3rkds" else 2
+        assert cnt["tucker_ops"] == 3 * 2 * per and cnt["kronsum_actions"] == 3 * 2
+        if fused:
+            assert cnt["gemm_launches"] == 3 and cnt["other_launches"] == 0
+        c.close()
+    ref, _ = etd.integrate(prob, scheme, 3 * tau, 3, steps=3)
+    for k in range(2):
+        assert relerr(out[True][k], out[False][k]) < 1e-13
+        assert relerr(out[True][k], ref[k]) < 1e-12
+
+
+def test_fused_small_step_n(kx):
+    """kx_step_n runs all steps in one launch on the fused path: equal to repeated kx_step."""
+    prob = inputs.make_problem("schnakenberg", 2, 64, seed=5)
+    res = []
+    for multi in (True, False):
+        c = kx.Context(0)
+        setup_problem(c, prob, "etd2rkds", 1.0 / 3000)
+        U = [dev(u) for u in prob.U0]
+        c.reset_counters()
+        if multi:
+            c.step_n(U, 20)
+        else:
+            for _ in range(20):
+                c.step(U)
+        c.sync()
+        cnt = c.counters()
+        assert cnt["steps"] == 20 and cnt["tucker_ops"] == 20 * 2 * 2
+        if multi:
+            assert cnt["gemm_launches"] == 1
+        res.append([u.cpu().numpy() for u in U])
+        c.close()
+    for k in range(2):
+        assert np.array_equal(res[0][k], res[1][k])
+
+
+def test_fused_small_not_eligible_falls_back(kx):
+    """Grids outside the fused kernel's range (n_2 < 8, n > 64, dense A) take the general path."""
+    for n, dense in (([16, 7], False), ([65, 16], False), ([32, 32], True)):
+        prob = inputs.make_problem("schnakenberg", 2, n, seed=2)
+        c = kx.Context(0)
+        setup_problem(c, prob, "etd3rkds", 1e-3)
+        if dense:
+            c.set_kronsum_mode(True)
+        U = [dev(u) for u in prob.U0]
+        c.reset_counters()
+        c.step(U)
+        c.sync()
+        assert c.counters()["gemm_launches"] > 1
+        c.close()
