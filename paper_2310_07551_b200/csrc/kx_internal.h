@@ -87,6 +87,20 @@ struct StencilArgs {
 };
 cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream);
 
+// Fused G = g(U), F = K U + G for two species, d in {2, 3}, tridiagonal A_mu, n_1 even,
+// N < 2^30, 16-B aligned tensors (one GPU).
+struct GKronArgs {
+  int d = 0, model = 0;
+  int n[3] = {1, 1, 1};
+  int N = 0;
+  double p[8] = {};
+  const double* U[2] = {};
+  double* G[2] = {};
+  double* F[2] = {};
+  const double* tri[2][3] = {};   // [species][mu-1]: lo | di | up (3 n_mu doubles)
+};
+cudaError_t launch_g_kronsum(const GKronArgs& a, cudaStream_t stream);
+
 // Kernel K*5 (fused2d.cu): nsteps whole ETD2RKDS / exprk3ds_real steps of a small 2-D grid
 // (8 <= n2 <= kFusedNMax, n1 <= kFusedNMax, tridiagonal A_mu) in one 8-CTA cluster.
 constexpr int kFusedCluster = 8;

@@ -1,19 +1,51 @@
 // One-GPU step schedules (ETD2RKDS, exprk3ds) and their CUDA-graph capture / replay.
 #include "kx_ctx.h"
 
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 
 namespace kx::detail {
 
 // ---------------------------------------------------------------- time steps --------------
+// G = g(U); F = K(U, A) + G.  One fused pass (launch_g_kronsum) when both species have
+// tridiagonal A_mu on a 2-D / 3-D grid with even n_1; else the nonlinearity kernel and the
+// Kronecker-sum action (stencil or dense mode products).
+kx_status first_phase(kx_ctx* c, double* const* U) {
+  const int ns = c->ncomp;
+  bool fuse = ns == 2 && (c->d == 2 || c->d == 3) && c->tn[0] % 2 == 0 && c->tN < (1LL << 30) &&
+              all_tridiag(c, 0, ns);
+  for (int s = 0; s < ns && fuse; ++s)
+    fuse = ((reinterpret_cast<uintptr_t>(U[s]) | reinterpret_cast<uintptr_t>(c->G[s]) |
+             reinterpret_cast<uintptr_t>(c->F[s])) & 15) == 0;
+  if (!fuse) {
+    KX_TRY(nonlin(c, 0, U, c->G));
+    return kronsum_multi(c, 0, ns, U, c->F, 1.0, c->G);
+  }
+  kx::GKronArgs a;
+  a.d = c->d;
+  a.model = c->model;
+  a.N = (int)c->tN;
+  for (int mu = 0; mu < c->d; ++mu) a.n[mu] = (int)c->tn[mu];
+  for (int i = 0; i < 8; ++i) a.p[i] = c->params[i];
+  for (int s = 0; s < 2; ++s) {
+    a.U[s] = U[s];
+    a.G[s] = c->G[s];
+    a.F[s] = c->F[s];
+    for (int mu = 0; mu < c->d; ++mu) a.tri[s][mu] = c->A_tri[s][mu];
+  }
+  KX_TRY(run_other(c, [&] { return kx::launch_g_kronsum(a, c->cur); }));
+  c->cnt.mode_products += (long long)ns * c->d;
+  c->cnt.kronsum_actions += ns;
+  return KX_OK;
+}
+
 // exprk3ds_real, Algorithm 1 (d = 2) / Algorithm 2 (d > 2), P:2229-2264 / P:2302-2342,
 // fused schedule of SURVEY.md §3 CS2.  Groups: 0 = F (3T terms), 1 = D2 (T), 2 = D3 (T).
 kx_status enqueue_step_etd3(kx_ctx* c, double* const* U) {
   const int ns = c->ncomp;
   // G = g(t, U); F = K(U, A) + G
-  KX_TRY(nonlin(c, 0, U, c->G));
-  KX_TRY(kronsum_multi(c, 0, ns, U, c->F, 1.0, c->G));
+  KX_TRY(first_phase(c, U));
   // all 3T first/middle modes on F at once
   double* const* ws = nullptr;
   KX_TRY(group_modes(c, c->groups[0], 0, c->groups[0].nterms, c->F, c->groups[0].slot0, &ws));
@@ -37,8 +69,7 @@ kx_status enqueue_step_etd3(kx_ctx* c, double* const* U) {
 // ETD2RKDS (eq:ETD2RK with eq:phisplit).  Groups: 0 = F (phi_1), 1 = D (phi_2).
 kx_status enqueue_step_etd2(kx_ctx* c, double* const* U) {
   const int ns = c->ncomp;
-  KX_TRY(nonlin(c, 0, U, c->G));
-  KX_TRY(kronsum_multi(c, 0, ns, U, c->F, 1.0, c->G));
+  KX_TRY(first_phase(c, U));
   double* const* ws = nullptr;
   KX_TRY(group_modes(c, c->groups[0], 0, 1, c->F, c->groups[0].slot0, &ws));
   KX_TRY(last_mode_concat(c, ws, c->F, 1, c->stages[0].slot, c->stages[0].B, c->Us, 1.0, 1.0, U));

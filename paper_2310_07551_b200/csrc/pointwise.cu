@@ -193,6 +193,94 @@ __global__ void __launch_bounds__(256) kronsum_tridiag_kernel(const StencilArgs 
   }
 }
 
+// Fused first phase of a step (K*3 + K*2'): G = g(U) and F = K U + G for both species in one
+// pass over U.  Two consecutive points per thread with 16-B loads/stores; the i_1 neighbours
+// come from the adjacent lanes by warp shuffles, the i_2 / i_3 neighbour lines by 16-B loads
+// that hit L2 (the neighbouring lines are being read by the neighbouring warps).  HBM traffic:
+// U read once, G and F written once (48 B per point pair of species vs 80 B for the two
+// separate kernels).  Arithmetic identical to nonlin2_kernel + kronsum_tridiag_kernel.
+template <int D>
+__global__ void __launch_bounds__(256) g_kronsum_kernel(const GKronArgs a) {
+  const int n1 = a.n[0], n2 = a.n[1], n3 = D == 3 ? a.n[2] : 1;
+  const int npairs = a.N / 2;
+  const int lane = threadIdx.x & 31;
+  const double2* __restrict__ U2[2] = {reinterpret_cast<const double2*>(a.U[0]),
+                                       reinterpret_cast<const double2*>(a.U[1])};
+  for (int base = blockIdx.x * blockDim.x; base < npairs; base += gridDim.x * blockDim.x) {
+    const int q = base + threadIdx.x;
+    const bool live = q < npairs;
+    const int p = 2 * (live ? q : npairs - 1);
+    const int line = p / n1, i1 = p - line * n1;
+    const int i2 = D >= 2 ? line % n2 : 0, i3 = D == 3 ? line / n2 : 0;
+    double2 x[2];
+    x[0] = U2[0][p / 2];
+    x[1] = U2[1][p / 2];
+    double2 gv[2];
+    g_point(a.model, a.p, x[0].x, x[1].x, gv[0].x, gv[1].x);
+    g_point(a.model, a.p, x[0].y, x[1].y, gv[0].y, gv[1].y);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      // i_1 neighbours: x[p-1] is the previous lane's .y, x[p+2] the next lane's .x
+      double xm = __shfl_up_sync(0xffffffffu, x[s].y, 1);
+      double xp = __shfl_down_sync(0xffffffffu, x[s].x, 1);
+      if (lane == 0 && i1 > 0) xm = a.U[s][p - 1];
+      if (lane == 31 && i1 + 2 < n1) xp = a.U[s][p + 2];
+      double acc0 = 1.0 * gv[s].x, acc1 = 1.0 * gv[s].y;
+      // directions mu = d .. 2 (descending, as the dense path)
+      if (D == 3) {
+        const double* t = a.tri[s][2];
+        const double c_lo = t[i3], c_di = t[n3 + i3], c_up = t[2 * n3 + i3];
+        const int st = n1 * n2;
+        double v0 = c_di * x[s].x, v1 = c_di * x[s].y;
+        if (i3 > 0) {
+          const double2 y = U2[s][(p - st) / 2];
+          v0 = fma(c_lo, y.x, v0);
+          v1 = fma(c_lo, y.y, v1);
+        }
+        if (i3 + 1 < n3) {
+          const double2 y = U2[s][(p + st) / 2];
+          v0 = fma(c_up, y.x, v0);
+          v1 = fma(c_up, y.y, v1);
+        }
+        acc0 += v0;
+        acc1 += v1;
+      }
+      {
+        const double* t = a.tri[s][1];
+        const double c_lo = t[i2], c_di = t[n2 + i2], c_up = t[2 * n2 + i2];
+        double v0 = c_di * x[s].x, v1 = c_di * x[s].y;
+        if (i2 > 0) {
+          const double2 y = U2[s][(p - n1) / 2];
+          v0 = fma(c_lo, y.x, v0);
+          v1 = fma(c_lo, y.y, v1);
+        }
+        if (i2 + 1 < n2) {
+          const double2 y = U2[s][(p + n1) / 2];
+          v0 = fma(c_up, y.x, v0);
+          v1 = fma(c_up, y.y, v1);
+        }
+        acc0 += v0;
+        acc1 += v1;
+      }
+      {
+        const double* t = a.tri[s][0];
+        double v0 = t[n1 + i1] * x[s].x;
+        if (i1 > 0) v0 = fma(t[i1], xm, v0);
+        v0 = fma(t[2 * n1 + i1], x[s].y, v0);   // i1 + 1 < n1 always (n1 even)
+        double v1 = t[n1 + i1 + 1] * x[s].y;
+        v1 = fma(t[i1 + 1], x[s].x, v1);
+        if (i1 + 2 < n1) v1 = fma(t[2 * n1 + i1 + 1], xp, v1);
+        acc0 += v0;
+        acc1 += v1;
+      }
+      if (live) {
+        reinterpret_cast<double2*>(a.G[s])[p / 2] = gv[s];
+        reinterpret_cast<double2*>(a.F[s])[p / 2] = make_double2(acc0, acc1);
+      }
+    }
+  }
+}
+
 // NaN/Inf watchdog (SURVEY §5 failure detection): mon = {steps completed, first bad step (-1)}
 __global__ void watch_finite_kernel(const double* __restrict__ x, long long n, int* mon) {
   int bad = 0;
@@ -234,6 +322,15 @@ cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t s
     if (mode == 0) nonlin_scalar_kernel<0><<<grid, 256, 0, stream>>>(a);
     else nonlin_scalar_kernel<1><<<grid, 256, 0, stream>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_g_kronsum(const GKronArgs& a, cudaStream_t stream) {
+  if (a.N <= 0) return cudaSuccess;
+  const int grid = grid_for(a.N / 2, 256);
+  if (a.d == 2) g_kronsum_kernel<2><<<grid, 256, 0, stream>>>(a);
+  else if (a.d == 3) g_kronsum_kernel<3><<<grid, 256, 0, stream>>>(a);
+  else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 
