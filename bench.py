@@ -216,6 +216,28 @@ def load_peak():
         return None, None
 
 
+def hbm_peak():
+    """HBM copy bandwidth of this pool (driver-written MEASURED_PEAKS.json), else ours."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"
+    except Exception:
+        _, h = load_peak()
+        return h, "profiles/peaks_r01.json hbm_copy_gbs"
+
+
+def elementwise_roofline(prof):
+    """Aggregate HBM roofline of the non-GEMM kernels (fused G/F pass, D = g(U_s) - G, ...):
+    algorithmic bytes (whole-field reads + writes) / their event-timed duration."""
+    if not prof.get("other_ms") or not prof.get("other_bytes"):
+        return None
+    peak, src = hbm_peak()
+    ach = prof["other_bytes"] / prof["other_ms"] / 1e6
+    return {"bound": "hbm", "kernels": "g_kronsum (G = g(U), F = K U + G), nonlinearity D = g(U_s) - G",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak if peak else None,
+            "peak_source": src, "ms_total": prof["other_ms"]}
+
+
 def load_traffic(cfg_name):
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
@@ -540,6 +562,7 @@ def main():
                      "gemm_share_of_step": prof["gemm_ms"] / (res["prof_ms"] * args.steps),
                      "instrumented_ms_per_step": res["prof_ms"],
                      "gemm_launches_per_step": gemm_launches / args.steps},
+        "elementwise_roofline": elementwise_roofline(prof),
         "step_tflops": step_flops / res["ms"] / 1e9,
         "gpu_launches": launches,
         "clocks": res["clocks"],

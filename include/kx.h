@@ -185,6 +185,10 @@ kx_status kx_check_finite(kx_ctx *ctx, const double *X);
 kx_status kx_set_profiling(kx_ctx *ctx, int on);
 kx_status kx_get_profile(kx_ctx *ctx, double *gemm_ms, double *other_ms, long long *gemm_launches,
                          long long *other_launches, double *gemm_flops);
+/* Algorithmic HBM bytes (reads + writes of whole fields) of the non-GEMM kernels timed since
+ * profiling was enabled (nonlinearity, stencil, fused G/F pass, watchdog): divided by
+ * other_ms of kx_get_profile it is their achieved bandwidth. */
+kx_status kx_get_profile_hbm(kx_ctx *ctx, double *other_bytes);
 /* Copy one phi-matrix of the current bank to the host (column-major n_mu x n_mu, unscaled):
  * phi_{l_term}(c tau alpha_{term,mu} A^comp_mu) for (ell, stage) as in kx_phi_apply.  For
  * KX_ETD3RKDS_CPLX, `term` indexes real planes: 2i = Re, 2i+1 = Im of term i. */

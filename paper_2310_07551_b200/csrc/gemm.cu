@@ -532,7 +532,7 @@ struct TileChoice {
   double eff;
 };
 // Resident CTAs per SM (register/smem-limited) and relative per-SM efficiency of each config.
-constexpr TileChoice kTiles[3] = {{128, 128, 32, 1, 1.00}, {128, 64, 16, 2, 0.95}, {64, 64, 16, 3, 0.90}};
+constexpr TileChoice kTiles[3] = {{128, 128, 32, 1, 1.00}, {128, 64, 16, 2, 0.85}, {64, 64, 16, 3, 0.80}};
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
 struct Prepared {
@@ -686,10 +686,15 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   // Tile choice: minimise (waves x per-wave work) / efficiency on the SM count.  With the
   // stream-K tail (k-tiles >= 8) a partial last wave costs only its fraction (+3% fix-up).
   const int nsm = num_sms();
+  static const TileChoice* tiles = [] {   // KX_GEMM_EFF="e0,e1,e2": tuning experiments only
+    static TileChoice t[3] = {kTiles[0], kTiles[1], kTiles[2]};
+    if (const char* e = getenv("KX_GEMM_EFF")) sscanf(e, "%lf,%lf,%lf", &t[0].eff, &t[1].eff, &t[2].eff);
+    return t;
+  }();
   int best = 0;
   double best_cost = 1e300;
   for (int i = 0; i < 3; ++i) {
-    const TileChoice& c = kTiles[i];
+    const TileChoice& c = tiles[i];
     const double tiles = (double)((g.M + c.bm - 1) / c.bm) * ((g.N + c.bn - 1) / c.bn) * nz;
     const double slots = (double)nsm * c.occ;
     double waves = std::ceil(tiles / slots);

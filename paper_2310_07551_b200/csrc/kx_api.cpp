@@ -490,6 +490,7 @@ kx_status kx_set_profiling(kx_ctx* c, int on) {
   c->prof_ms[0] = c->prof_ms[1] = 0;
   c->prof_launches[0] = c->prof_launches[1] = 0;
   c->prof_flops = 0;
+  c->prof_bytes = 0;
   return KX_OK;
 }
 
@@ -502,6 +503,13 @@ kx_status kx_get_profile(kx_ctx* c, double* gemm_ms, double* other_ms, long long
   if (gemm_launches) *gemm_launches = c->prof_launches[0];
   if (other_launches) *other_launches = c->prof_launches[1];
   if (gemm_flops) *gemm_flops = c->prof_flops;
+  return KX_OK;
+}
+
+kx_status kx_get_profile_hbm(kx_ctx* c, double* other_bytes) {
+  if (!c) return KX_ERR_INVALID;
+  KX_TRY(collect_profile(c));
+  if (other_bytes) *other_bytes = c->prof_bytes;
   return KX_OK;
 }
 

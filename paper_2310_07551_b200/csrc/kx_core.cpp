@@ -191,7 +191,8 @@ kx_status kronsum_multi(kx_ctx* c, int comp0, int ns, const double* const* X, do
         a.up[s][mu] = t + 2 * n;
       }
     }
-    KX_TRY(run_other(c, [&] { return kx::launch_kronsum_tridiag(a, c->cur); }));
+    const double bytes = 8.0 * (double)c->tN * ns * ((Dd && beta != 0.0) ? 3 : 2);
+    KX_TRY(run_other(c, [&] { return kx::launch_kronsum_tridiag(a, c->cur); }, bytes));
     c->cnt.mode_products += (long long)ns * c->d;
     c->cnt.kronsum_actions += ns;
     return KX_OK;
@@ -354,7 +355,9 @@ kx_status nonlin(kx_ctx* c, int mode, const double* const* u, double* const* out
     a.G[s] = c->G[s];
   }
   for (int i = 0; i < 8; ++i) a.p[i] = c->params[i];
-  return run_other(c, [&] { return kx::launch_nonlinearity(a, mode, c->cur); });
+  // HBM bytes: read the ncomp fields (+ G for mode 1), write ncomp fields
+  const double bytes = 8.0 * (double)c->tN * c->ncomp * (mode == 1 ? 3 : 2);
+  return run_other(c, [&] { return kx::launch_nonlinearity(a, mode, c->cur); }, bytes);
 }
 
 kx_status collect_profile(kx_ctx* c) {
@@ -365,7 +368,7 @@ kx_status collect_profile(kx_ctx* c) {
     KX_CUDA(c, cudaEventElapsedTime(&ms, c->ev_pool[r.e0], c->ev_pool[r.e1]));
     c->prof_ms[r.cls] += ms;
     c->prof_launches[r.cls] += 1;
-    c->prof_flops += r.flops;
+    (r.cls == 0 ? c->prof_flops : c->prof_bytes) += r.flops;
   }
   c->recs.clear();
   c->ev_used = c->gexec ? c->graph_ev_end : 0;

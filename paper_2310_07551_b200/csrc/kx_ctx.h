@@ -172,6 +172,7 @@ struct kx_ctx {
   double prof_ms[2] = {0, 0};
   long long prof_launches[2] = {0, 0};
   double prof_flops = 0;
+  double prof_bytes = 0;        // algorithmic HBM bytes of the non-GEMM kernels
 };
 
 namespace kx::detail {
@@ -220,7 +221,7 @@ kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* sr
 kx_status nonlin(kx_ctx* c, int mode, const double* const* u, double* const* out);
 kx_status check_ptr(kx_ctx* c, const void* p, const char* what);
 template <class F>
-kx_status run_other(kx_ctx* c, F&& launch) {
+kx_status run_other(kx_ctx* c, F&& launch, double bytes = 0.0) {
   int e0 = -1;
   if (c->profiling) {
     e0 = c->ev_used;
@@ -230,7 +231,7 @@ kx_status run_other(kx_ctx* c, F&& launch) {
   KX_CUDA(c, launch());
   if (c->profiling) {
     KX_CUDA(c, record(c, pool_event(c, e0 + 1)));
-    c->recs.push_back({1, e0, e0 + 1, 0.0});
+    c->recs.push_back({1, e0, e0 + 1, bytes});
   }
   c->cnt.other_launches += 1;
   return KX_OK;

@@ -34,7 +34,8 @@ kx_status first_phase(kx_ctx* c, double* const* U) {
     a.F[s] = c->F[s];
     for (int mu = 0; mu < c->d; ++mu) a.tri[s][mu] = c->A_tri[s][mu];
   }
-  KX_TRY(run_other(c, [&] { return kx::launch_g_kronsum(a, c->cur); }));
+  // HBM bytes: read U (2 fields), write G and F (4 fields)
+  KX_TRY(run_other(c, [&] { return kx::launch_g_kronsum(a, c->cur); }, 48.0 * (double)c->tN));
   c->cnt.mode_products += (long long)ns * c->d;
   c->cnt.kronsum_actions += ns;
   return KX_OK;
@@ -83,7 +84,8 @@ kx_status enqueue_step_etd2(kx_ctx* c, double* const* U) {
 kx_status enqueue_watch(kx_ctx* c, double* const* U) {
   if (!c->nan_check) return KX_OK;
   for (int s = 0; s < c->ncomp; ++s)
-    KX_TRY(run_other(c, [&] { return kx::launch_watch_finite(U[s], c->tN, c->watch, c->cur); }));
+    KX_TRY(run_other(c, [&] { return kx::launch_watch_finite(U[s], c->tN, c->watch, c->cur); },
+                     8.0 * (double)c->tN));
   return run_other(c, [&] { return kx::launch_watch_tick(c->watch, c->cur); });
 }
 
@@ -242,7 +244,7 @@ kx_status step_impl(kx_ctx* c, double* const* U) {
       KX_CUDA(c, cudaEventElapsedTime(&ms, c->ev_pool[r.e0], c->ev_pool[r.e1]));
       c->prof_ms[r.cls] += ms;
       c->prof_launches[r.cls] += 1;
-      c->prof_flops += r.flops;
+      (r.cls == 0 ? c->prof_flops : c->prof_bytes) += r.flops;
     }
   }
   return KX_OK;

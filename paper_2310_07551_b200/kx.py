@@ -76,6 +76,7 @@ _SIGS = {
     "kx_set_nan_check": (_i, [_vp, _i]),
     "kx_set_profiling": (_i, [_vp, _i]),
     "kx_get_profile": (_i, [_vp, _dp, _dp, C.POINTER(_ll), C.POINTER(_ll), _dp]),
+    "kx_get_profile_hbm": (_i, [_vp, _dp]),
     "kx_get_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
     "kx_scheme_coefficients": (_i, [_i, _i, _i, C.POINTER(_i), _dp, C.POINTER(_i), _dp]),
     "kx_scheme_coefficients_cplx": (_i, [_i, _i, C.POINTER(_i), _dp, _dp, C.POINTER(_i), _dp, _dp]),
@@ -279,8 +280,10 @@ class Context:
         gl, ol = C.c_longlong(), C.c_longlong()
         self._check(kx_get_profile(self.h, C.byref(gm), C.byref(om), C.byref(gl), C.byref(ol),
                                    C.byref(gf)))
+        ob = C.c_double()
+        self._check(kx_get_profile_hbm(self.h, C.byref(ob)))
         return dict(gemm_ms=gm.value, other_ms=om.value, gemm_launches=gl.value,
-                    other_launches=ol.value, gemm_flops=gf.value)
+                    other_launches=ol.value, gemm_flops=gf.value, other_bytes=ob.value)
 
     def phi_matrix(self, comp: int, ell: int, stage: int, term: int, mu: int) -> np.ndarray:
         n = self.n[mu - 1]
