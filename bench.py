@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
     ap.add_argument("--no-extras", action="store_true", help="skip Tucker sweep / e2e / cpu leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="sharded mode: producers store straight into the peers' receive buffers "
+                         "(CUDA IPC, NCCL only as a barrier), or NCCL all-to-alls")
     ap.add_argument("--no-overlap", action="store_true",
                     help="sharded mode: one exchange per phase instead of term-by-term overlap")
     ap.add_argument("--scheme", default=None, choices=["etd2rkds", "etd3rkds", "exprk3ds_cplx"],
@@ -382,6 +385,14 @@ def run_kx(args, rank, world, sharded):
         t0 = time.perf_counter()
         ctx.set_tau(tau, cfg["scheme"])
         phi_s = time.perf_counter() - t0
+        if args.exchange == "p2p":
+            # direct peer stores: every rank maps the others' receive buffers (CUDA IPC)
+            blobs = [ctx.ipc_export()]
+            if world > 1:
+                allb = [None] * world
+                dist.all_gather_object(allb, blobs[0])
+                blobs = allb
+            ctx.ipc_import(blobs)
     else:
         prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=rank)
         ctx, phi_s = setup_ctx(kx, prob, cfg["scheme"], tau, stream)
@@ -547,7 +558,9 @@ def main():
         "data": "synthetic (seeded SplitMix64 initial data, FD Neumann Laplacians; inputs/)",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "grid": prob.n, "species": 2,
                    "scheme": cfg["scheme"], "tau": cfg["T"] / cfg["m"],
-                   "parallelism": (f"slab-sharded x{world} along i_d (NCCL all-to-all)" if sharded
+                   "parallelism": ((f"slab-sharded x{world} along i_d ("
+                                    + ("direct peer stores over NVLink + NCCL barrier" if args.exchange == "p2p"
+                                       else "NCCL all-to-all") + ")") if sharded
                                    else ("replicas" if world > 1 else "single GPU")),
                    "l2": "256 MiB buffer written between timed steps (L2 flushed)"},
         "roofline": {"bound": "tensor", "kernel": "mode-product GEMM (fp64 DMMA mma.sync.m8n8k4)",

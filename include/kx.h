@@ -35,6 +35,8 @@
 #ifndef KX_H
 #define KX_H
 
+#include <stddef.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -166,6 +168,19 @@ kx_status kx_create_group(kx_ctx **ctxs, int nranks, int device, void *cuda_stre
  * (SURVEY §8(f) f2); off = one exchange per phase on the context stream. */
 kx_status kx_set_dist_overlap(kx_ctx *ctx, int on);
 kx_status kx_step_group(kx_ctx *const *ctxs, int nranks, double t, double *const *U);
+/* Direct peer stores: the kernel producing each exchanged tensor (stencil F,
+ * nonlinearity D, the last mode product of every term group) stores block q of its
+ * peer-packed output straight into rank q's receive buffer, so the all-to-all becomes a barrier
+ * (stream order in a loopback group; a 1-double NCCL all-reduce across processes).  Real
+ * schemes with tridiagonal A_mu; other cases keep the exchanges.  Loopback group: enable after
+ * every member's kx_set_tau (which disables it again). */
+kx_status kx_group_set_p2p(kx_ctx *const *ctxs, int nranks, int on);
+/* NCCL ranks (one process per GPU): export this rank's receive buffers as CUDA IPC handles
+ * (blob == NULL: *len = size needed), all-gather the blobs (e.g. torch.distributed), then
+ * import all nranks blobs (rank order, len_each bytes each) on every rank.  After kx_set_tau,
+ * which disables it; every rank must import before the next kx_step. */
+kx_status kx_dist_ipc_export(kx_ctx *ctx, void *blob, size_t cap, size_t *len);
+kx_status kx_dist_ipc_import(kx_ctx *ctx, const void *blobs, size_t len_each);
 
 /* ---------------------------------------------------------------- utilities -------- */
 kx_status kx_get_counters(const kx_ctx *ctx, kx_counters *out);

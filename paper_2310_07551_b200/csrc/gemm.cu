@@ -309,17 +309,18 @@ struct GemmTile {
           }
           if (m == n) v0 += diag;
           if (m == n + 1) v1 += diag;
-          *reinterpret_cast<double2*>(C + (long long)m * p.ldc + n) = make_double2(v0, v1);
+          *reinterpret_cast<double2*>(peer_redirect(p.peer, cd.s, C + (long long)m * p.ldc + n)) =
+              make_double2(v0, v1);
         } else {
           if (D) v0 += beta * D[(long long)m * p.ldd + n];
           if (E) v0 += gamma * E[(long long)m * p.lde + n];
           if (m == n) v0 += diag;
-          C[(long long)m * p.ldc + n] = v0;
+          *peer_redirect(p.peer, cd.s, C + (long long)m * p.ldc + n) = v0;
           if (n + 1 < N) {
             if (D) v1 += beta * D[(long long)m * p.ldd + n + 1];
             if (E) v1 += gamma * E[(long long)m * p.lde + n + 1];
             if (m == n + 1) v1 += diag;
-            C[(long long)m * p.ldc + n + 1] = v1;
+            *peer_redirect(p.peer, cd.s, C + (long long)m * p.ldc + n + 1) = v1;
           }
         }
       }
@@ -525,6 +526,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     T_::zero(acc);
   }
   cp_async_wait<0>();
+  if (p.peer.P) __threadfence_system();   // peer stores performed before the kernel completes
 }
 
 struct TileChoice {

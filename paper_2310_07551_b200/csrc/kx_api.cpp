@@ -629,12 +629,16 @@ kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const
     c->cur = c->stream;
   }
   const int nc = ctxs[0]->ncomp;
+  for (int r = 0; r < nranks; ++r)
+    if (ctxs[r]->p2p != ctxs[0]->p2p)
+      return fail(ctxs[0], KX_ERR_INVALID, "direct peer stores are on for some members only: call kx_group_set_p2p after kx_set_tau");
   std::vector<Exchange> xs(nranks);
   for (int ph = 0; ph < dist_phases(ctxs[0]); ++ph) {
     for (int r = 0; r < nranks; ++r) KX_TRY(dist_phase(ctxs[r], U + (size_t)r * nc, ph, xs[r]));
     // loopback exchanges: device copies on the shared stream, after every rank's phase
     for (int r = 0; r < nranks; ++r) {
       const Exchange& xr = xs[r];
+      if (xr.kind == 2) continue;   // the producers stored straight into the peers
       if (xr.kind == 1) {   // halo: first plane -> rank-1's upper halo, last plane -> rank+1's lower
         for (int k = 0; k + 1 < xr.nbuf; k += 2) {
           if (r > 0)
@@ -656,6 +660,93 @@ kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const
     KX_TRY(enqueue_watch(ctxs[r], U + (size_t)r * nc));
     ctxs[r]->cnt.steps += 1;
   }
+  return KX_OK;
+}
+
+kx_status kx_group_set_p2p(kx_ctx* const* ctxs, int nranks, int on) {
+  if (!ctxs || nranks < 1 || nranks > kx::kMaxPeers) return KX_ERR_INVALID;
+  for (int r = 0; r < nranks; ++r) {
+    kx_ctx* c = ctxs[r];
+    if (!c || c->dist != 2 || c->rank != r || c->nranks != nranks) return KX_ERR_INVALID;
+    if (on && !c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
+  }
+  for (int r = 0; r < nranks; ++r) {
+    kx_ctx* c = ctxs[r];
+    p2p_close(c);
+    if (!on) continue;
+    for (int q = 0; q < nranks; ++q)
+      for (int s = 0; s < c->ncomp; ++s) {
+        c->peerRA[q][s] = ctxs[q]->RA[s];
+        c->peerFB[q][s] = ctxs[q]->F_B[s];
+        c->peerDB[q][s] = ctxs[q]->D_B[s];
+        c->peerHlo[q][s] = ctxs[q]->halo_lo[s];
+        c->peerHhi[q][s] = ctxs[q]->halo_hi[s];
+      }
+    c->p2p = 1;
+  }
+  return KX_OK;
+}
+
+// Receive buffers of this rank as CUDA IPC handles, in the fixed order (RA, F_B, D_B,
+// halo_lo, halo_hi) x component.
+static const int kIpcBufs = 5;
+static double** ipc_slot(kx_ctx* c, int k, int s) {
+  switch (k) {
+    case 0: return &c->RA[s];
+    case 1: return &c->F_B[s];
+    case 2: return &c->D_B[s];
+    case 3: return &c->halo_lo[s];
+    default: return &c->halo_hi[s];
+  }
+}
+
+kx_status kx_dist_ipc_export(kx_ctx* c, void* blob, size_t cap, size_t* len) {
+  if (!c || !len) return KX_ERR_INVALID;
+  if (c->dist != 1) return fail(c, KX_ERR_INVALID, "not an NCCL-distributed context");
+  if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
+  const size_t need = (size_t)kIpcBufs * c->ncomp * sizeof(cudaIpcMemHandle_t);
+  *len = need;
+  if (!blob) return KX_OK;
+  if (cap < need) return fail(c, KX_ERR_INVALID, "blob too small");
+  auto* h = static_cast<cudaIpcMemHandle_t*>(blob);
+  for (int k = 0; k < kIpcBufs; ++k)
+    for (int s = 0; s < c->ncomp; ++s)
+      KX_CUDA(c, cudaIpcGetMemHandle(&h[k * c->ncomp + s], *ipc_slot(c, k, s)));
+  return KX_OK;
+}
+
+kx_status kx_dist_ipc_import(kx_ctx* c, const void* blobs, size_t len_each) {
+  if (!c || !blobs) return KX_ERR_INVALID;
+  if (c->dist != 1) return fail(c, KX_ERR_INVALID, "not an NCCL-distributed context");
+  if (c->nranks > kx::kMaxPeers) return fail(c, KX_ERR_UNSUPPORTED, "more ranks than kMaxPeers");
+  if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
+  const size_t need = (size_t)kIpcBufs * c->ncomp * sizeof(cudaIpcMemHandle_t);
+  if (len_each != need) return fail(c, KX_ERR_INVALID, "blob size mismatch");
+  p2p_close(c);
+  for (int q = 0; q < c->nranks; ++q) {
+    const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(static_cast<const char*>(blobs) + q * need);
+    for (int k = 0; k < kIpcBufs; ++k)
+      for (int s = 0; s < c->ncomp; ++s) {
+        double* p = nullptr;
+        if (q == c->rank) {
+          p = *ipc_slot(c, k, s);
+        } else {
+          void* m = nullptr;
+          cudaError_t e = cudaIpcOpenMemHandle(&m, h[k * c->ncomp + s], cudaIpcMemLazyEnablePeerAccess);
+          if (e != cudaSuccess) {
+            cudaGetLastError();
+            p2p_close(c);
+            return fail(c, KX_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+          }
+          c->ipc_open.push_back(m);
+          p = static_cast<double*>(m);
+        }
+        double* (*dst)[MAXS] = k == 0 ? c->peerRA : k == 1 ? c->peerFB : k == 2 ? c->peerDB
+                             : k == 3 ? c->peerHlo : c->peerHhi;
+        dst[q][s] = p;
+      }
+  }
+  c->p2p = 1;
   return KX_OK;
 }
 

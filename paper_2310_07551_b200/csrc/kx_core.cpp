@@ -78,6 +78,7 @@ void drop_graph(kx_ctx* c) {
 
 void drop_bank(kx_ctx* c) {
   drop_graph(c);
+  p2p_close(c);   // the peers' mappings point at buffers about to be reallocated
   free_list(c->bank_allocs);
   free_list(c->ws_allocs);
   c->groups.clear();
@@ -217,7 +218,7 @@ kx_status kronsum_multi(kx_ctx* c, int comp0, int ns, const double* const* X, do
 // [t0, t0+nt) of group gi applied to inputs X[s]; results land in slots [slot, slot+nt) of
 // the returned workspace (W1 or W2).
 kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* const* X,
-                      int slot, double* const** out_ws) {
+                      int slot, double* const** out_ws, const kx::PeerMap* peer) {
   const int d = c->d;
   const long long N = c->tN;
   const int ns = c->ncomp;
@@ -239,6 +240,10 @@ kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* c
       g.A[s] = G.first[s] + t0 * nd;
       g.B[s] = X[s];
       g.C[s] = c->W1[s] + (long long)slot * N;
+    }
+    if (peer && d == 2) {   // the final product of the group: store straight into the peers
+      g.peer = *peer;
+      for (int s = 0; s < ns; ++s) g.peer.local_base[s] = c->W1[s];
     }
     KX_TRY(run_gemm(c, g));
   }
@@ -304,6 +309,10 @@ kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* c
       g.A[s] = G.mid[s][mu - 1] + t0 * nm * nm;
       g.B[s] = cur[s] + (long long)slot * N;
       g.C[s] = nxt[s] + (long long)slot * N;
+    }
+    if (peer && mu == 2) {   // the final product of the group: store straight into the peers
+      g.peer = *peer;
+      for (int s = 0; s < ns; ++s) g.peer.local_base[s] = nxt[s];
     }
     KX_TRY(run_gemm(c, g));
     std::swap(cur, nxt);

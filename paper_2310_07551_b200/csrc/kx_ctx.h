@@ -158,6 +158,16 @@ struct kx_ctx {
   double* halo_lo[MAXS] = {};   // tridiagonal K on a slab: the neighbours' boundary planes of U
   double* halo_hi[MAXS] = {};
   double* F_pack[MAXS] = {};
+  // direct peer stores instead of exchanges (kx_group_set_p2p / kx_dist_ipc_import): every
+  // rank's receive buffers, [rank][component]; valid until the workspaces are reallocated
+  int p2p = 0;
+  double* peerRA[kx::kMaxPeers][MAXS] = {};
+  double* peerFB[kx::kMaxPeers][MAXS] = {};
+  double* peerDB[kx::kMaxPeers][MAXS] = {};
+  double* peerHlo[kx::kMaxPeers][MAXS] = {};
+  double* peerHhi[kx::kMaxPeers][MAXS] = {};
+  std::vector<void*> ipc_open;   // CUDA IPC mappings of the peers' buffers
+  double* bar_buf = nullptr;     // scratch of the NCCL barrier
 
   int nan_check = 0;             // per-step NaN/Inf watchdog inside the step graph
   int* watch = nullptr;          // device {steps completed, first bad step or -1}
@@ -214,7 +224,7 @@ bool all_tridiag(const kx_ctx* c, int comp0, int ns);
 kx_status kronsum_multi(kx_ctx* c, int comp0, int ns, const double* const* X, double* const* Y,
                         double beta, const double* const* Dd);
 kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* const* X,
-                      int slot, double* const** out_ws);
+                      int slot, double* const** out_ws, const kx::PeerMap* peer = nullptr);
 kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
                            const int* slots, double* const* B, double* const* Y, double alpha,
                            double beta, const double* const* Dd);
@@ -258,6 +268,8 @@ struct NcclApi {
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 #endif
   std::string why;
@@ -269,7 +281,7 @@ NcclApi& nccl();   // dlopen'ed once (the NCCL torch already loaded)
 // first plane) goes to rank-1 and lands in its recv[2s+1]; send[2s+1] (last plane) goes to
 // rank+1 and lands in its recv[2s]; the global end ranks skip the missing side.
 struct Exchange {
-  int kind = 0;
+  int kind = 0;   // 0 all-to-all, 1 halo, 2 none (direct peer stores: only a barrier)
   int nbuf = 0;
   size_t count = 0;
   const double* send[64];
@@ -281,6 +293,8 @@ struct Exchange {
   }
 };
 void set_layout(kx_ctx* c, bool B);
+bool p2p_on(const kx_ctx* c);
+void p2p_close(kx_ctx* c);
 kx_status dist_f_source(kx_ctx* c, double* const* U, Exchange& x);
 kx_status dist_f_build(kx_ctx* c);
 bool dist_banded(const kx_ctx* c);

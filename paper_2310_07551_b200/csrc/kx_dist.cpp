@@ -36,8 +36,9 @@ NcclApi& nccl() {
   api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
   api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
   api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+  api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
   api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv &&
-           api.GroupStart && api.GroupEnd && api.GetErrorString;
+           api.GroupStart && api.GroupEnd && api.GetErrorString && api.AllReduce;
   if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
 #else
   api.why = "built without nccl.h";
@@ -45,6 +46,36 @@ NcclApi& nccl() {
   return api;
 }
 
+
+// ---- direct peer stores (P2P mode) ------------------------------------------------------
+// The producing kernel of every exchange stores block q of its peer-packed output straight
+// into rank q's receive buffer (kx::PeerMap); an exchange then reduces to a barrier between
+// the producing and the consuming phase (stream order in an in-process group, a one-double
+// NCCL all-reduce across processes).  Real schemes with the tridiagonal (halo) schedule.
+bool dist_banded(const kx_ctx* c);
+bool p2p_on(const kx_ctx* c) { return c->p2p && !c->cplx && dist_banded(c); }
+
+void p2p_close(kx_ctx* c) {
+  for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  c->ipc_open.clear();
+  c->p2p = 0;
+  for (int q = 0; q < kx::kMaxPeers; ++q)
+    for (int s = 0; s < MAXS; ++s)
+      c->peerRA[q][s] = c->peerFB[q][s] = c->peerDB[q][s] = c->peerHlo[q][s] = c->peerHhi[q][s] = nullptr;
+}
+
+kx::PeerMap peer_map(const kx_ctx* c, double* const (*peers)[MAXS], double* const* local) {
+  kx::PeerMap pm;
+  pm.P = c->nranks;
+  pm.rank = c->rank;
+  pm.chunk = c->Nloc / c->nranks;
+  pm.span = c->Nloc;
+  for (int s = 0; s < c->ncomp; ++s) {
+    pm.local_base[s] = local ? local[s] : nullptr;
+    for (int q = 0; q < c->nranks; ++q) pm.peer_base[s][q] = peers[q][s];
+  }
+  return pm;
+}
 
 void set_layout(kx_ctx* c, bool B) {
   for (int mu = 0; mu < KX_MAXD; ++mu) c->tn[mu] = B ? c->nB[mu] : c->nA[mu];
@@ -120,6 +151,12 @@ kx_status dist_group(kx_ctx* c, int gi, double* const* Xb, Exchange& x) {
   set_layout(c, true);
   const Group& G = c->groups[gi];
   double* const* ws = nullptr;
+  if (p2p_on(c)) {   // the final mode product stores every term slot straight into the peers
+    const kx::PeerMap pm = peer_map(c, c->peerRA, nullptr);
+    KX_TRY(group_modes(c, G, 0, G.nterms, Xb, G.slot0, &ws, &pm));
+    x.kind = 2;
+    return KX_OK;
+  }
   if (c->dist == 1 && c->overlap && c->comm) {
     // f2: modes d..2 term by term; each term's slots go to the peers on the comm stream while
     // the next term's mode products run; the compute stream joins before the stage GEMM
@@ -199,7 +236,12 @@ kx_status dist_d_source(kx_ctx* c, Exchange& x) {
     a.G[s] = c->G[s];
   }
   for (int i = 0; i < 8; ++i) a.p[i] = c->params[i];
+  if (p2p_on(c)) a.peer = peer_map(c, c->peerDB, c->D_pack);
   KX_TRY(run_other(c, [&] { return kx::launch_nonlinearity(a, 1, c->cur); }));
+  if (p2p_on(c)) {
+    x.kind = 2;
+    return KX_OK;
+  }
   x.count = (size_t)(c->Nloc / c->nranks);
   for (int s = 0; s < c->ncomp; ++s) x.add(c->D_pack[s], c->D_B[s]);
   return KX_OK;
@@ -217,6 +259,17 @@ kx_status dist_f_halo(kx_ctx* c, double* const* U, Exchange& x) {
   KX_TRY(nonlin(c, 0, U, c->G));
   const long long ndl = c->nA[c->d - 1];
   const long long plane = c->Nloc / ndl;
+  if (p2p_on(c)) {   // boundary planes straight into the neighbours' halo buffers (copy engine)
+    for (int s = 0; s < c->ncomp; ++s) {
+      if (c->rank > 0)
+        KX_CUDA(c, cudaMemcpyAsync(c->peerHhi[c->rank - 1][s], U[s], plane * 8, cudaMemcpyDeviceToDevice, c->cur));
+      if (c->rank + 1 < c->nranks)
+        KX_CUDA(c, cudaMemcpyAsync(c->peerHlo[c->rank + 1][s], U[s] + (ndl - 1) * plane, plane * 8,
+                                   cudaMemcpyDeviceToDevice, c->cur));
+    }
+    x.kind = 2;
+    return KX_OK;
+  }
   x.kind = 1;
   x.count = (size_t)plane;
   for (int s = 0; s < c->ncomp; ++s) {
@@ -253,9 +306,14 @@ kx_status dist_f_stencil(kx_ctx* c, double* const* U, Exchange& x) {
       a.up[s][mu] = t + 2 * n;
     }
   }
+  if (p2p_on(c)) a.peer = peer_map(c, c->peerFB, c->F_pack);
   KX_TRY(run_other(c, [&] { return kx::launch_kronsum_tridiag(a, c->cur); }));
   c->cnt.mode_products += (long long)c->ncomp * c->d;
   c->cnt.kronsum_actions += c->ncomp;
+  if (p2p_on(c)) {
+    x.kind = 2;
+    return KX_OK;
+  }
   x.count = (size_t)(c->Nloc / c->nranks);
   for (int s = 0; s < c->ncomp; ++s) x.add(c->F_pack[s], c->F_B[s]);
   return KX_OK;
@@ -314,6 +372,15 @@ kx_status nccl_exchange(kx_ctx* c, const Exchange& x, cudaStream_t st) {
     if (r != ncclSuccess) return fail(c, KX_ERR_NCCL, std::string("NCCL: ") + api.GetErrorString(r));
     return KX_OK;
   };
+  if (x.kind == 2) {   // direct peer stores: every rank's producers are done before anyone reads
+    if (c->nranks == 1) return KX_OK;
+    if (!c->bar_buf) {
+      std::vector<double*> keep;
+      KX_TRY(dalloc(c, &c->bar_buf, 1, keep));
+      KX_CUDA(c, cudaMemsetAsync(c->bar_buf, 0, 8, st));
+    }
+    return chk(api.AllReduce(c->bar_buf, c->bar_buf, 1, ncclFloat64, ncclSum, comm, st));
+  }
   KX_TRY(chk(api.GroupStart()));
   if (x.kind == 1) {
     for (int k = 0; k + 1 < x.nbuf; k += 2) {
@@ -347,7 +414,7 @@ kx_status dist_step_nccl(kx_ctx* c, double* const* U) {
   Exchange x;
   for (int ph = 0; ph < dist_phases(c); ++ph) {
     KX_TRY(dist_phase(c, U, ph, x));
-    if (x.nbuf) KX_TRY(nccl_exchange(c, x, c->cur));
+    if (x.nbuf || x.kind == 2) KX_TRY(nccl_exchange(c, x, c->cur));
   }
   KX_TRY(enqueue_watch(c, U));
   c->cnt.steps += 1;

@@ -17,6 +17,28 @@ constexpr int MAXSEG = 64;     // K segments of a concatenated-K last-mode produ
 // A layout COL ("m contiguous"): A_z(m, k) = A[k*lda + m]
 // B_z(k, n) = B[k*ldb + n];  C/D/E row-major with ldc/ldd/lde.
 // X_z = X_s[s] + t*sX_t + b*sX_b for X in {A, B, C, D, E}.
+// Direct peer stores (the all-to-all of the slab decomposition fused into the producing
+// kernel): a kernel whose output is a peer-packed send buffer (P blocks of
+// `chunk` doubles per `span`-long slot) instead stores block q straight into peer q's receive
+// buffer at block `rank` — the receive layout the all-to-all would have produced.  peer_base
+// are device pointers valid in this process (same-device buffers of an in-process group, or
+// CUDA IPC mappings of the peers' buffers).
+constexpr int kMaxPeers = 8;
+struct PeerMap {
+  int P = 0;                       // 0: plain local stores
+  int rank = 0;
+  long long chunk = 0, span = 0;
+  const double* local_base[MAXS] = {};
+  double* peer_base[MAXS][kMaxPeers] = {};
+};
+__device__ __forceinline__ double* peer_redirect(const PeerMap& pm, int s, double* ptr) {
+  if (pm.P == 0) return ptr;
+  const long long off = ptr - pm.local_base[s];
+  const long long slot = off / pm.span, within = off - slot * pm.span;
+  const long long q = within / pm.chunk;
+  return pm.peer_base[s][q] + slot * pm.span + pm.rank * pm.chunk + (within - q * pm.chunk);
+}
+
 struct GemmArgs {
   int M = 0, N = 0, kseg = 0, nseg = 1;
   bool arow = true;
@@ -34,6 +56,7 @@ struct GemmArgs {
   // stream-K scratch (library-owned, per context): kSkSlots x 128 x 128 doubles + flags
   double* sk_ws = nullptr;
   int* sk_flags = nullptr;
+  PeerMap peer;                    // epilogue stores redirected to peers (P > 0)
 };
 constexpr int kSkSlots = 304;    // partial-tile slots of 128x128 doubles (>= 2 x SM count)
 constexpr int kSkFlags = 2048;   // counters: a pair per split tile
@@ -58,6 +81,7 @@ struct PointwiseArgs {
   // optional peer-packed output (distributed contexts): point (row, i1) of a row-major
   // (N/n1) x n1 slab goes to out[q*(N/P) + row*n1l + i1 - q*n1l], q = i1 / n1l, n1l = n1/P
   long long pack_n1 = 0, pack_n1l = 0;
+  PeerMap peer;                    // packed output stored straight into the peers (P > 0)
 };
 cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t stream);
 
@@ -84,6 +108,7 @@ struct StencilArgs {
   const double* halo_hi[MAXS] = {};
   // optional peer-packed output, as PointwiseArgs::pack_*
   long long pack_n1 = 0, pack_n1l = 0;
+  PeerMap peer;
 };
 cudaError_t launch_kronsum_tridiag(const StencilArgs& a, cudaStream_t stream);
 

@@ -43,9 +43,10 @@ __global__ void __launch_bounds__(256) nonlin2_kernel(const PointwiseArgs a) {
       r2.y -= h2.y;
     }
     const long long oi = out_index(a, 2 * i) / 2;   // pairs never straddle a peer block
-    o1[oi] = r1;
-    o2[oi] = r2;
+    *reinterpret_cast<double2*>(peer_redirect(a.peer, 0, reinterpret_cast<double*>(o1 + oi))) = r1;
+    *reinterpret_cast<double2*>(peer_redirect(a.peer, 1, reinterpret_cast<double*>(o2 + oi))) = r2;
   }
+  if (a.peer.P) __threadfence_system();
 }
 
 template <int MODE>
@@ -60,11 +61,12 @@ __global__ void __launch_bounds__(256) nonlin_scalar_kernel(const PointwiseArgs 
         r2 -= a.G[1][i];
       }
       const long long oi = out_index(a, i);
-      a.out[0][oi] = r1;
-      a.out[1][oi] = r2;
+      *peer_redirect(a.peer, 0, a.out[0] + oi) = r1;
+      *peer_redirect(a.peer, 1, a.out[1] + oi) = r2;
     } else {
       const long long oi = out_index(a, i);
-      for (int c = 0; c < a.ncomp; ++c) a.out[c][oi] = MODE == 1 ? -a.G[c][i] : 0.0;   // g = 0 (KX_MODEL_NONE)
+      for (int c = 0; c < a.ncomp; ++c)   // g = 0 (KX_MODEL_NONE)
+        *peer_redirect(a.peer, c, a.out[c] + oi) = MODE == 1 ? -a.G[c][i] : 0.0;
     }
   }
 }
@@ -187,10 +189,11 @@ __global__ void __launch_bounds__(256) kronsum_tridiag_kernel(const StencilArgs 
           const I q = i1 / n1l;
           o = q * (N / n1 * n1l) + line * n1l + (i1 - q * n1l);
         }
-        Y[o] = v[u];
+        *peer_redirect(a.peer, s, Y + o) = v[u];
       }
     }
   }
+  if (a.peer.P) __threadfence_system();
 }
 
 // Fused first phase of a step (K*3 + K*2'): G = g(U) and F = K U + G for both species in one

@@ -68,6 +68,9 @@ _SIGS = {
     "kx_create_dist": (_i, [C.POINTER(_vp), _i, _vp, _vp, _i, _i]),
     "kx_create_group": (_i, [C.POINTER(_vp), _i, _i, _vp]),
     "kx_step_group": (_i, [C.POINTER(_vp), _i, _d, C.POINTER(_vp)]),
+    "kx_group_set_p2p": (_i, [C.POINTER(_vp), _i, _i]),
+    "kx_dist_ipc_export": (_i, [_vp, _vp, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "kx_dist_ipc_import": (_i, [_vp, _vp, C.c_size_t]),
     "kx_set_dist_overlap": (_i, [_vp, _i]),
     "kx_get_counters": (_i, [_vp, C.POINTER(kx_counters)]),
     "kx_reset_counters": (_i, [_vp]),
@@ -235,6 +238,21 @@ class Context:
         arr = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
         self._check(kx_step_n(self.h, t0, nsteps, arr))
 
+    def ipc_export(self) -> bytes:
+        """This NCCL rank's receive buffers as CUDA IPC handles (after set_tau)."""
+        n = C.c_size_t()
+        self._check(kx_dist_ipc_export(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        self._check(kx_dist_ipc_export(self.h, buf, n.value, C.byref(n)))
+        return buf.raw
+
+    def ipc_import(self, blobs: list):
+        """Every rank's ipc_export() blob, in rank order: enables direct peer stores."""
+        each = len(blobs[0])
+        assert all(len(b) == each for b in blobs)
+        joined = C.create_string_buffer(b"".join(blobs), each * len(blobs))
+        self._check(kx_dist_ipc_import(self.h, joined, each))
+
     def set_fused_small(self, on: bool):
         self._check(kx_set_fused_small(self.h, 1 if on else 0))
 
@@ -314,6 +332,12 @@ class Group:
         flat = [_ptr(u) for Ur in U for u in Ur]
         arr = (C.c_void_p * len(flat))(*flat)
         st = kx_step_group(self._arr, self.nranks, t, arr)
+        if st != KX_OK:
+            raise KxError(st, kx_last_error(self.ctx[0].h).decode())
+
+    def set_p2p(self, on: bool):
+        """Direct peer stores instead of exchange copies (after every member's set_tau)."""
+        st = kx_group_set_p2p(self._arr, self.nranks, 1 if on else 0)
         if st != KX_OK:
             raise KxError(st, kx_last_error(self.ctx[0].h).decode())
 

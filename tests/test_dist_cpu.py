@@ -161,3 +161,60 @@ def test_slab_decomposition_gloo(case):
         assert p.exitcode == 0
     for rank, err in res:
         assert err <= 1e-13, (rank, err)
+
+
+# ---------------------------------------------------------------- direct peer stores --------
+def peer_redirect(off, P, rank, chunk, span):
+    """Where the library's kx::peer_redirect (kx_internal.h) sends element `off` of a
+    peer-packed send buffer: (destination rank, offset in its receive buffer)."""
+    slot, within = divmod(off, span)
+    q = within // chunk
+    return q, slot * span + rank * chunk + (within - q * chunk)
+
+
+def _p2p_worker(rank, world, port, nslots, nloc, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        chunk = nloc // world
+        rs = np.random.default_rng(rank)
+        send = rs.standard_normal(nslots * nloc)
+        # reference: the exchange the NCCL path performs, per slot an all-to-all of chunks
+        ref = np.empty_like(send)
+        for s in range(nslots):
+            blk = torch.from_numpy(send[s * nloc:(s + 1) * nloc].copy())
+            out = torch.empty_like(blk)
+            dist.all_to_all_single(out, blk)
+            ref[s * nloc:(s + 1) * nloc] = out.numpy()
+        # direct stores: every rank scatters its elements to (q, offset); gather what lands here
+        allsend = [torch.empty(nslots * nloc, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(allsend, torch.from_numpy(send))
+        got = np.full_like(send, np.nan)
+        for r in range(world):
+            src = allsend[r].numpy()
+            for off in range(src.size):
+                dq, doff = peer_redirect(off, world, r, chunk, nloc)
+                if dq == rank:
+                    assert np.isnan(got[doff])      # every receive element is written once
+                    got[doff] = src[off]
+        q.put((rank, bool(np.array_equal(got, ref))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_direct_peer_stores_equal_all_to_all_gloo(world):
+    """The direct-peer-store address map writes exactly the receive buffers the slot-wise
+    all-to-all produces (each element once)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, 3, 8 * world, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok in res), res

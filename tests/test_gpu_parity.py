@@ -350,7 +350,8 @@ def slab(u, n, r, P):
                                   ("schnakenberg", 2, [64, 64], "etd2rkds", 0.25 / 3000, 4),
                                   ("fhn", 3, [16, 12, 8], "etd2rkds", 0.01, 2)])
 @pytest.mark.parametrize("dense_kronsum", [False, True], ids=["halo-stencil", "dense-kronsum"])
-def test_sharded_step_loopback(kx, case, dense_kronsum):
+@pytest.mark.parametrize("p2p", [False, True], ids=["exchange-copies", "direct-peer-stores"])
+def test_sharded_step_loopback(kx, case, dense_kronsum, p2p):
     """The slab-sharded schedule (layouts A/B, peer-packed all-to-alls, concat-K over
     (term, source rank) segments; the Kronecker sum either as a stencil with a halo exchange
     of the boundary planes or as dense mode products across layouts) on an in-process loopback
@@ -364,6 +365,8 @@ def test_sharded_step_loopback(kx, case, dense_kronsum):
     for c in grp.ctx:
         setup_problem(c, prob, scheme, tau)
         c.set_kronsum_mode(dense_kronsum)
+    if p2p:   # the producers store straight into the other ranks' receive buffers
+        grp.set_p2p(True)
     Ug = [[dev(slab(prob.U0[s], n, r, P)) for s in range(2)] for r in range(P)]
     steps = 3
     for k in range(steps):
@@ -672,3 +675,47 @@ def test_fused_small_not_eligible_falls_back(kx):
         c.sync()
         assert c.counters()["gemm_launches"] > 1
         c.close()
+
+
+def test_p2p_requires_every_member(kx):
+    """kx_set_tau disables direct peer stores on that member: the group refuses to step until
+    kx_group_set_p2p is called again (no stale peer pointers)."""
+    prob = inputs.make_problem("fhn", 3, [16, 12, 8], seed=7)
+    grp = kx.Group(2)
+    for c in grp.ctx:
+        setup_problem(c, prob, "etd3rkds", 0.015)
+    grp.set_p2p(True)
+    Ug = [[dev(slab(prob.U0[s], prob.n, r, 2)) for s in range(2)] for r in range(2)]
+    grp.step(Ug)
+    grp.ctx[1].set_tau(0.01, "etd3rkds")
+    with pytest.raises(kx.KxError, match="kx_group_set_p2p"):
+        grp.step(Ug)
+    grp.set_p2p(True)
+    grp.step(Ug)
+    grp.ctx[0].sync()
+    grp.close()
+
+
+def test_nccl_single_rank_ipc_p2p(kx):
+    """NCCL rank with direct peer stores (IPC export/import round trip on one rank; the
+    exchanges become barriers): equal to the single-GPU step to rounding."""
+    prob = inputs.make_problem("fhn", 3, [16, 12, 8], seed=7)
+    tau = 0.015
+    dctx = kx.Context(0, dist=(kx.nccl_unique_id(), 0, 1))
+    setup_problem(dctx, prob, "etd3rkds", tau)
+    blob = dctx.ipc_export()
+    assert len(blob) == 5 * 2 * 64
+    dctx.ipc_import([blob])
+    one = kx.Context(0)
+    setup_problem(one, prob, "etd3rkds", tau)
+    Ud = [dev(u) for u in prob.U0]
+    U1 = [dev(u) for u in prob.U0]
+    for _ in range(3):
+        dctx.step(Ud)
+        one.step(U1)
+    dctx.sync()
+    one.sync()
+    for s in range(2):
+        assert relerr(Ud[s].cpu().numpy(), U1[s].cpu().numpy()) <= 1e-13
+    dctx.close()
+    one.close()
