@@ -143,7 +143,9 @@ kx_status kx_integrate_host(kx_ctx *ctx, double t0, int nsteps, double *const *U
 /* Small 2-D grids (d = 2, 8 <= n_2 <= 64, n_1 <= 64, tridiagonal A_mu, real scheme, one GPU):
  * on = 1 (default) executes each step as ONE kernel on an 8-CTA thread-block cluster that
  * keeps the state in shared memory and fuses the mode-2 and mode-1 products of every term
- * (the shape of eq:exp2d; SURVEY §2 K*5); on = 0 forces the general path. */
+ * (the shape of eq:exp2d; SURVEY §2 K*5); and kx_tucker on a 2-D grid with
+ * n_1, n_2 <= 128 runs both mode products in one launch (intermediate in shared memory).
+ * on = 0 forces the general path for both. */
 kx_status kx_set_fused_small(kx_ctx *ctx, int on);
 
 /* ---------------------------------------------------------------- multi-GPU -------- */

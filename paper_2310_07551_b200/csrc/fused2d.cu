@@ -258,3 +258,116 @@ cudaError_t launch_fused2d(const Fused2dArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace kx
+
+// ---------------------------------------------------------------------------------------
+// A single small 2-D Tucker operator in one launch ("1 fused for d=2 small
+// n", eq:exp2d P:240-250):  Y = alpha L_2 X L_1^T + beta Y  for n_1, n_2 <= 128.  CTA c forms
+// rows I = [8c, 8c+8) of Y: it stages the whole X (<= 128 x 128) in shared memory, computes
+// Z_I = L_2[I,:] X (one m8 fragment row block, kept in shared memory) and then Y_I = Z_I L_1^T;
+// the operands of L are read from L2 once per product.  The intermediate never reaches HBM and
+// the two mode products are one launch of ceil(n_2/8) CTAs.
+namespace kx {
+namespace {
+constexpr int TS_NMAX = 128;
+constexpr int TS_SS = TS_NMAX + 4;   // = 4 mod 16 doubles
+constexpr int TS_NT = 256;
+
+__global__ void __launch_bounds__(TS_NT) tucker2d_small_kernel(const double* __restrict__ X, double* Y,
+                                                               const double* __restrict__ L1,
+                                                               const double* __restrict__ L2, int n1, int n2,
+                                                               double alpha, double beta) {
+  extern __shared__ __align__(16) double ts_smem[];
+  double(*Xs)[TS_SS] = reinterpret_cast<double(*)[TS_SS]>(ts_smem);   // X, then L1^T
+  double(*Zs)[TS_SS] = reinterpret_cast<double(*)[TS_SS]>(ts_smem + TS_NMAX * TS_SS);
+  double(*As)[TS_SS] = reinterpret_cast<double(*)[TS_SS]>(ts_smem + (TS_NMAX + 8) * TS_SS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int r0 = blockIdx.x * 8, r = min(8, n2 - r0);
+  const int n1p = (n1 + 7) & ~7, n2p = (n2 + 3) & ~3, n1q = (n1 + 3) & ~3;
+  // stage X (rows < n2p, columns < n1p, zero padded) and the rows I of L2 in shared memory
+  // a row-major n_rows x n1 matrix into the padded tile, 16-B loads when n1 is even
+  auto stage = [&](const double* __restrict__ src, int rows, int rows_p) {
+    if ((n1 & 1) == 0) {
+      const int h = n1p / 2;
+#pragma unroll 4
+      for (int i = tid; i < rows_p * h; i += TS_NT) {
+        const int row = i / h, col = 2 * (i - row * h);
+        const double2 v = (row < rows && col < n1)
+                              ? __ldg(reinterpret_cast<const double2*>(src + (long long)row * n1 + col))
+                              : make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(&Xs[row][col]) = v;
+      }
+    } else {
+#pragma unroll 4
+      for (int i = tid; i < rows_p * n1p; i += TS_NT) {
+        const int row = i / n1p, col = i - row * n1p;
+        Xs[row][col] = (row < rows && col < n1) ? __ldg(src + (long long)row * n1 + col) : 0.0;
+      }
+    }
+  };
+  stage(X, n2, n2p);
+  for (int i = tid; i < 8 * n2p; i += TS_NT) {
+    const int k = i / 8, m = i - k * 8;   // column-major L2: consecutive threads, consecutive rows
+    As[m][k] = (m < r && k < n2) ? L2[(long long)k * n2 + r0 + m] : 0.0;
+  }
+  __syncthreads();
+  const int nf = n1p / 8;   // n-fragments of 8 columns: warp w takes w, w+8
+  double z[2][2] = {};
+  for (int kk = 0; kk < n2p; kk += 4) {
+    const double av = As[g][kk + t4];
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int j = warp + 8 * f;
+      if (j < nf) dmma(z[f][0], z[f][1], av, Xs[kk + t4][j * 8 + g]);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int j = warp + 8 * f;
+    if (j < nf) {
+      Zs[g][j * 8 + 2 * t4] = z[f][0];
+      Zs[g][j * 8 + 2 * t4 + 1] = z[f][1];
+    }
+  }
+  __syncthreads();
+  // stage L1^T (L1's column-major buffer read row-major) over X
+  stage(L1, n1, n1q);
+  __syncthreads();
+  double y[2][2] = {};
+  for (int kk = 0; kk < n1q; kk += 4) {
+    const double zv = Zs[g][kk + t4];
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int j = warp + 8 * f;
+      if (j < nf) dmma(y[f][0], y[f][1], zv, Xs[kk + t4][j * 8 + g]);
+    }
+  }
+  if (g < r) {
+    double* yr = Y + (long long)(r0 + g) * n1;
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int c0 = (warp + 8 * f) * 8 + 2 * t4;
+      if (c0 < n1) yr[c0] = alpha * y[f][0] + (beta != 0.0 ? beta * yr[c0] : 0.0);
+      if (c0 + 1 < n1) yr[c0 + 1] = alpha * y[f][1] + (beta != 0.0 ? beta * yr[c0 + 1] : 0.0);
+    }
+  }
+}
+}  // namespace
+
+bool tucker2d_small_fits(long long n1, long long n2) {
+  return n1 >= 1 && n2 >= 1 && n1 <= TS_NMAX && n2 <= TS_NMAX;
+}
+
+cudaError_t launch_tucker2d_small(const double* X, double* Y, const double* L1, const double* L2, int n1,
+                                  int n2, double alpha, double beta, cudaStream_t stream) {
+  const size_t smem = (size_t)(TS_NMAX + 16) * TS_SS * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tucker2d_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  tucker2d_small_kernel<<<(n2 + 7) / 8, TS_NT, smem, stream>>>(X, Y, L1, L2, n1, n2, alpha, beta);
+  return cudaGetLastError();
+}
+
+}  // namespace kx

@@ -258,6 +258,26 @@ kx_status kx_tucker(kx_ctx* c, const double* X, double* Y, const double* const* 
   if (X == Y) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
   c->cur = c->stream;
   const int d = c->d;
+  if (d == 2 && c->fused_small && kx::tucker2d_small_fits(c->tn[0], c->tn[1])) {
+    // small 2-D grid: both mode products in one launch, the intermediate in shared memory
+    const double fl = 2.0 * (double)c->tN * (double)(c->tn[0] + c->tn[1]);
+    int e0 = -1;
+    if (c->profiling) {
+      e0 = c->ev_used;
+      c->ev_used += 2;
+      KX_CUDA(c, record(c, pool_event(c, e0)));
+    }
+    KX_CUDA(c, kx::launch_tucker2d_small(X, Y, L[0], L[1], (int)c->tn[0], (int)c->tn[1], alpha, beta, c->cur));
+    if (c->profiling) {
+      KX_CUDA(c, record(c, pool_event(c, e0 + 1)));
+      c->recs.push_back({0, e0, e0 + 1, fl});
+    }
+    c->cnt.gemm_launches += 1;
+    c->cnt.mode_products += 2;
+    c->cnt.mode_product_flops += fl;
+    c->cnt.tucker_ops += 1;
+    return KX_OK;
+  }
   const double* src = X;
   double* bufs[2] = {c->tmp1, c->tmp2};
   int w = 0;

@@ -144,6 +144,10 @@ struct Fused2dArgs {
   long long* prof = nullptr;                   // diagnostics: clock64 phase stamps (<= 64)
 };
 cudaError_t launch_fused2d(const Fused2dArgs& a, cudaStream_t stream);
+// One d = 2 Tucker operator Y = alpha L2 X L1^T + beta Y in one launch (n_1, n_2 <= 128).
+bool tucker2d_small_fits(long long n1, long long n2);
+cudaError_t launch_tucker2d_small(const double* X, double* Y, const double* L1, const double* L2, int n1,
+                                  int n2, double alpha, double beta, cudaStream_t stream);
 size_t fused2d_smem_bytes();
 
 // Y = alpha * X (elementwise, n doubles); used for bank assembly.

@@ -719,3 +719,28 @@ def test_nccl_single_rank_ipc_p2p(kx):
         assert relerr(Ud[s].cpu().numpy(), U1[s].cpu().numpy()) <= 1e-13
     dctx.close()
     one.close()
+
+
+@pytest.mark.parametrize("n", [[64, 64], [128, 128], [1, 7], [7, 1], [33, 100], [128, 9], [5, 128]],
+                         ids=lambda n: "x".join(map(str, n)))
+def test_tucker2d_small_one_launch(kx, n):
+    """d = 2, n <= 128: the Tucker operator as one launch (intermediate in shared memory),
+    with alpha/beta, against the oracle and against the general two-launch path."""
+    x = tensor(n, 31)
+    Ls = [inputs.uniform_sym(40 + mu, 0, m * m).reshape(m, m) / math.sqrt(m) for mu, m in enumerate(n)]
+    y0 = tensor(n, 32)
+    out = {}
+    for fused in (True, False):
+        c = kx.Context(0)
+        c.set_grid(n, 1)
+        c.set_fused_small(fused)
+        Y = dev(y0)
+        c.reset_counters()
+        c.tucker(dev(x), Y, [dmat(L) for L in Ls], alpha=0.5, beta=-2.0)
+        c.sync()
+        assert c.counters()["gemm_launches"] == (1 if fused else 2)
+        out[fused] = Y.cpu().numpy()
+        c.close()
+    ref = 0.5 * vec(tucker(unvec(x, n), Ls)) - 2.0 * y0
+    assert relerr(out[True], ref) <= 1e-12
+    assert relerr(out[True], out[False]) <= 1e-13
