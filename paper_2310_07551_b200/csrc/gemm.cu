@@ -166,7 +166,7 @@ __device__ __forceinline__ int sk_slot(const Sched& sc, int i, long long t0u) {
   return 2 * i + (sk_begin(sc, i) >= t0u ? 0 : 1);
 }
 
-template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 struct GemmTile {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   static constexpr int NT = C_::NT, SA = C_::SA, SB = C_::SB, A_ST = C_::A_ST, B_ST = C_::B_ST;
@@ -178,10 +178,11 @@ struct GemmTile {
   };
 
   __device__ __forceinline__ static Coord coords(const GemmArgs& p, const Sched& sc, long long tl) {
-    const long long tmn = (long long)sc.tiles_m * sc.tiles_n;
-    const long long zq = tl / tmn;
+    // 32-bit arithmetic: tile counts stay far below 2^31
+    const unsigned tmn = (unsigned)sc.tiles_m * (unsigned)sc.tiles_n;
+    const unsigned zq = (unsigned)tl / tmn;
     const int z = (int)zq;
-    const int r = (int)(tl - zq * tmn);
+    const int r = (int)((unsigned)tl - zq * tmn);
     int tm, tn;
     if (sc.m_fastest) {
       tm = r % sc.tiles_m;
@@ -276,6 +277,11 @@ struct GemmTile {
     }
   };
 
+  __device__ __forceinline__ static double* out_ptr(const GemmArgs& p, int s, double* q) {
+    if constexpr (PEER) return peer_redirect(p.peer, s, q);
+    else return q;
+  }
+
   // C = alpha*acc + beta*D + gamma*E + diag*[m==n]
   __device__ __forceinline__ static void epilogue(const GemmArgs& p, const Coord& cd,
                                                   const double (&acc)[FM][FN][2], unsigned mask) {
@@ -287,6 +293,25 @@ struct GemmTile {
     const double* D = p.D[cd.s] ? p.D[cd.s] + cd.t * p.sD_t + cd.b * p.sD_b : nullptr;
     const double* E = p.E[cd.s] ? p.E[cd.s] + cd.t * p.sE_t + cd.b * p.sE_b : nullptr;
     const double alpha = p.alpha, beta = p.beta, gamma = p.gamma, diag = p.diag;
+    if constexpr (VEC == 2) {
+      // fast paths for whole interior tiles (every launch of the large configs): no bounds
+      // checks, row pointers hoisted, the D loads issued before the stores
+      const bool plain = !PEER && mask == ~0u && !D && !E && diag == 0.0 && cd.m0 + BM <= M &&
+                         cd.n0 + BN <= N;
+      if (plain) {
+        const long long ls = 8 * p.ldc;
+        double* Cw = C + (long long)(cd.m0 + wm0 + g) * p.ldc + cd.n0 + wn0 + 2 * t4;
+        {
+#pragma unroll
+          for (int i = 0; i < FM; ++i)
+#pragma unroll
+            for (int j = 0; j < FN; ++j)
+              *reinterpret_cast<double2*>(Cw + i * ls + j * 8) =
+                  make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+          return;
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < FM; ++i) {
       const int m = cd.m0 + wm0 + i * 8 + g;
@@ -309,18 +334,18 @@ struct GemmTile {
           }
           if (m == n) v0 += diag;
           if (m == n + 1) v1 += diag;
-          *reinterpret_cast<double2*>(peer_redirect(p.peer, cd.s, C + (long long)m * p.ldc + n)) =
+          *reinterpret_cast<double2*>(out_ptr(p, cd.s, C + (long long)m * p.ldc + n)) =
               make_double2(v0, v1);
         } else {
           if (D) v0 += beta * D[(long long)m * p.ldd + n];
           if (E) v0 += gamma * E[(long long)m * p.lde + n];
           if (m == n) v0 += diag;
-          *peer_redirect(p.peer, cd.s, C + (long long)m * p.ldc + n) = v0;
+          *out_ptr(p, cd.s, C + (long long)m * p.ldc + n) = v0;
           if (n + 1 < N) {
             if (D) v1 += beta * D[(long long)m * p.ldd + n + 1];
             if (E) v1 += gamma * E[(long long)m * p.lde + n + 1];
             if (m == n + 1) v1 += diag;
-            *peer_redirect(p.peer, cd.s, C + (long long)m * p.ldc + n + 1) = v1;
+            *out_ptr(p, cd.s, C + (long long)m * p.ldc + n + 1) = v1;
           }
         }
       }
@@ -335,10 +360,10 @@ struct GemmTile {
   }
 };
 
-template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT)
     gemm_kernel(const GemmArgs p, const Sched sc) {
-  using T_ = GemmTile<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  using T_ = GemmTile<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
   using Coord = typename T_::Coord;
   constexpr int NT = T_::NT, FM = T_::FM, FN = T_::FN, SA = T_::SA, SB = T_::SB;
   constexpr int A_ST = T_::A_ST, B_ST = T_::B_ST;
@@ -526,7 +551,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     T_::zero(acc);
   }
   cp_async_wait<0>();
-  if (p.peer.P) __threadfence_system();   // peer stores performed before the kernel completes
+  if constexpr (PEER) __threadfence_system();   // peer stores performed before the kernel completes
 }
 
 struct TileChoice {
@@ -536,18 +561,18 @@ struct TileChoice {
 // Resident CTAs per SM (register/smem-limited) and relative per-SM efficiency of each config.
 constexpr TileChoice kTiles[3] = {{128, 128, 32, 1, 1.00}, {128, 64, 16, 2, 0.85}, {64, 64, 16, 3, 0.80}};
 
-template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 struct Prepared {
   static inline bool done = false;
   static inline int occ = 1;   // resident CTAs per SM (occupancy API)
 };
 
-template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 cudaError_t prepare_cfg() {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
   if (!P_::done) {
-    auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+    auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -561,11 +586,11 @@ cudaError_t prepare_cfg() {
 
 int num_sms();
 
-template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES>
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>();
+  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
+  cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
   if (e != cudaSuccess) return e;
   Sched sc;
   sc.tiles_m = (g.M + BM - 1) / BM;
@@ -617,14 +642,17 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES>, g, sc);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
   }
-  gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc);
+  gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc);
   return cudaGetLastError();
 }
 
 template <bool AROW, int VEC>
 cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
+  // direct peer stores (sharded steps, large shapes): the 128 x 128 configuration only, in its
+  // own instantiation so the redirect arithmetic costs the plain kernels no registers
+  if (g.peer.P) return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
   switch (which) {
     case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>(g, nz, stream);
     case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
@@ -635,6 +663,7 @@ cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t str
 template <bool AROW, int VEC>
 void prepare_layout() {
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>();
+  prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>();
   prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>();
   prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>();
 }
