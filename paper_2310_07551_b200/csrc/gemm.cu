@@ -296,12 +296,12 @@ struct GemmTile {
     if constexpr (VEC == 2) {
       // fast paths for whole interior tiles (every launch of the large configs): no bounds
       // checks, row pointers hoisted, the D loads issued before the stores
-      const bool plain = !PEER && mask == ~0u && !D && !E && diag == 0.0 && cd.m0 + BM <= M &&
+      const bool plain = !PEER && mask == ~0u && !E && diag == 0.0 && cd.m0 + BM <= M &&
                          cd.n0 + BN <= N;
       if (plain) {
         const long long ls = 8 * p.ldc;
         double* Cw = C + (long long)(cd.m0 + wm0 + g) * p.ldc + cd.n0 + wn0 + 2 * t4;
-        {
+        if (!D) {
 #pragma unroll
           for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -310,6 +310,19 @@ struct GemmTile {
                   make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
           return;
         }
+        const long long ld = 8 * p.ldd;
+        const double* Dw = D + (long long)(cd.m0 + wm0 + g) * p.ldd + cd.n0 + wn0 + 2 * t4;
+#pragma unroll
+        for (int i = 0; i < FM; ++i) {
+          double2 dv[FN];   // one fragment row of D in flight at a time (register budget)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dv[j] = *reinterpret_cast<const double2*>(Dw + i * ld + j * 8);
+#pragma unroll
+          for (int j = 0; j < FN; ++j)
+            *reinterpret_cast<double2*>(Cw + i * ls + j * 8) =
+                make_double2(alpha * acc[i][j][0] + beta * dv[j].x, alpha * acc[i][j][1] + beta * dv[j].y);
+        }
+        return;
       }
     }
 #pragma unroll
