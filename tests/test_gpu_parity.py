@@ -748,3 +748,38 @@ def test_tucker2d_small_one_launch(kx, n):
     ref = 0.5 * vec(tucker(unvec(x, n), Ls)) - 2.0 * y0
     assert relerr(out[True], ref) <= 1e-12
     assert relerr(out[True], out[False]) <= 1e-13
+
+
+@pytest.mark.parametrize("scheme", ["etd2rkds", "etd3rkds"])
+def test_fused_small_single_component_linear(kx, scheme):
+    """One component, no reaction (u' = K u, K = A_2 (+) A_1 Neumann Laplacians): the fused
+    small-grid kernel with a single species equals the general path (1e-13) and tracks the
+    exact exp(t K) u0 (scipy expm of the assembled K) to the splitting error."""
+    import scipy.linalg
+    from oracle.tensor import kronsum_assemble
+    n = [24, 16]
+    A = [inputs.laplacian_neumann(m, 1.0, 0.5) for m in n]
+    u0 = inputs.kron_vec([inputs.cosine_mode(n[0], 2), inputs.cosine_mode(n[1], 1)]) + 0.3
+    tau, steps = 1e-3, 10
+    out = {}
+    for fused in (True, False):
+        c = kx.Context(0)
+        c.set_grid(n, 1)
+        for mu in range(2):
+            c.set_direction_matrix(0, mu + 1, A[mu])
+        c.set_model("none")
+        c.set_tau(tau, scheme)
+        c.set_fused_small(fused)
+        U = [dev(u0)]
+        c.reset_counters()
+        for _ in range(steps):
+            c.step(U)
+        c.sync()
+        if fused:
+            assert c.counters()["gemm_launches"] == steps
+        out[fused] = U[0].cpu().numpy()
+        c.close()
+    assert relerr(out[True], out[False]) <= 1e-13
+    K = kronsum_assemble(A)
+    exact = scipy.linalg.expm(steps * tau * K) @ u0
+    assert relerr(out[True], exact) <= (1e-5 if scheme == "etd2rkds" else 1e-6)
