@@ -207,6 +207,116 @@ __global__ void __launch_bounds__(256) g_kronsum_kernel(const GKronArgs a) {
   const int n1 = a.n[0], n2 = a.n[1], n3 = D == 3 ? a.n[2] : 1;
   const int npairs = a.N / 2;
   const int lane = threadIdx.x & 31;
+  const double2* __restrict__ U0 = reinterpret_cast<const double2*>(a.U[0]);
+  const double2* __restrict__ U1 = reinterpret_cast<const double2*>(a.U[1]);
+  double2* __restrict__ G0 = reinterpret_cast<double2*>(a.G[0]);
+  double2* __restrict__ G1 = reinterpret_cast<double2*>(a.G[1]);
+  double2* __restrict__ F0 = reinterpret_cast<double2*>(a.F[0]);
+  double2* __restrict__ F1 = reinterpret_cast<double2*>(a.F[1]);
+  const int st3 = n1 * n2;
+  for (int base = blockIdx.x * blockDim.x; base < npairs; base += gridDim.x * blockDim.x) {
+    const int q = base + threadIdx.x;
+    const bool live = q < npairs;
+    const int h = live ? q : npairs - 1;   // pair index (points 2h, 2h+1)
+    const int p = 2 * h;
+    const int line = p / n1, i1 = p - line * n1;
+    const int i2 = line % n2, i3 = D == 3 ? line / n2 : 0;
+    const bool l2 = i2 > 0, u2 = i2 + 1 < n2, l3 = D == 3 && i3 > 0, u3 = D == 3 && i3 + 1 < n3;
+    // every load of the pair first (no store in between: all loads in flight together)
+    const double2 zero = make_double2(0.0, 0.0);
+    double2 x[2], ym2[2], yp2[2], ym3[2], yp3[2];
+    x[0] = U0[h];
+    x[1] = U1[h];
+    ym2[0] = l2 ? U0[h - n1 / 2] : zero;
+    ym2[1] = l2 ? U1[h - n1 / 2] : zero;
+    yp2[0] = u2 ? U0[h + n1 / 2] : zero;
+    yp2[1] = u2 ? U1[h + n1 / 2] : zero;
+    if (D == 3) {
+      ym3[0] = l3 ? U0[h - st3 / 2] : zero;
+      ym3[1] = l3 ? U1[h - st3 / 2] : zero;
+      yp3[0] = u3 ? U0[h + st3 / 2] : zero;
+      yp3[1] = u3 ? U1[h + st3 / 2] : zero;
+    }
+    double xm[2], xp[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      // i_1 neighbours: x[p-1] is the previous lane's .y, x[p+2] the next lane's .x
+      xm[s] = __shfl_up_sync(0xffffffffu, x[s].y, 1);
+      xp[s] = __shfl_down_sync(0xffffffffu, x[s].x, 1);
+      if (lane == 0 && i1 > 0) xm[s] = a.U[s][p - 1];
+      if (lane == 31 && i1 + 2 < n1) xp[s] = a.U[s][p + 2];
+    }
+    double2 gv[2];
+    g_point(a.model, a.p, x[0].x, x[1].x, gv[0].x, gv[1].x);
+    g_point(a.model, a.p, x[0].y, x[1].y, gv[0].y, gv[1].y);
+    double2 f[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      double acc0 = 1.0 * gv[s].x, acc1 = 1.0 * gv[s].y;
+      // directions mu = d .. 2 (descending, as the dense path)
+      if (D == 3) {
+        const double* __restrict__ t = a.tri[s][2];
+        const double c_di = t[n3 + i3];
+        double v0 = c_di * x[s].x, v1 = c_di * x[s].y;
+        if (l3) {
+          const double c = t[i3];
+          v0 = fma(c, ym3[s].x, v0);
+          v1 = fma(c, ym3[s].y, v1);
+        }
+        if (u3) {
+          const double c = t[2 * n3 + i3];
+          v0 = fma(c, yp3[s].x, v0);
+          v1 = fma(c, yp3[s].y, v1);
+        }
+        acc0 += v0;
+        acc1 += v1;
+      }
+      {
+        const double* __restrict__ t = a.tri[s][1];
+        const double c_di = t[n2 + i2];
+        double v0 = c_di * x[s].x, v1 = c_di * x[s].y;
+        if (l2) {
+          const double c = t[i2];
+          v0 = fma(c, ym2[s].x, v0);
+          v1 = fma(c, ym2[s].y, v1);
+        }
+        if (u2) {
+          const double c = t[2 * n2 + i2];
+          v0 = fma(c, yp2[s].x, v0);
+          v1 = fma(c, yp2[s].y, v1);
+        }
+        acc0 += v0;
+        acc1 += v1;
+      }
+      {
+        const double* __restrict__ t = a.tri[s][0];
+        double v0 = t[n1 + i1] * x[s].x;
+        if (i1 > 0) v0 = fma(t[i1], xm[s], v0);
+        v0 = fma(t[2 * n1 + i1], x[s].y, v0);   // i1 + 1 < n1 always (n1 even)
+        double v1 = t[n1 + i1 + 1] * x[s].y;
+        v1 = fma(t[i1 + 1], x[s].x, v1);
+        if (i1 + 2 < n1) v1 = fma(t[2 * n1 + i1 + 1], xp[s], v1);
+        acc0 += v0;
+        acc1 += v1;
+      }
+      f[s] = make_double2(acc0, acc1);
+    }
+    if (live) {
+      G0[h] = gv[0];
+      G1[h] = gv[1];
+      F0[h] = f[0];
+      F1[h] = f[1];
+    }
+  }
+}
+
+// d = 3 variant: one species at a time (fewer live registers: 64, no spills at full
+// occupancy; the all-loads-first form of g_kronsum_kernel needs 80)
+template <int D>
+__global__ void __launch_bounds__(256) g_kronsum_seq_kernel(const GKronArgs a) {
+  const int n1 = a.n[0], n2 = a.n[1], n3 = D == 3 ? a.n[2] : 1;
+  const int npairs = a.N / 2;
+  const int lane = threadIdx.x & 31;
   const double2* __restrict__ U2[2] = {reinterpret_cast<const double2*>(a.U[0]),
                                        reinterpret_cast<const double2*>(a.U[1])};
   for (int base = blockIdx.x * blockDim.x; base < npairs; base += gridDim.x * blockDim.x) {
@@ -332,7 +442,7 @@ cudaError_t launch_g_kronsum(const GKronArgs& a, cudaStream_t stream) {
   if (a.N <= 0) return cudaSuccess;
   const int grid = grid_for(a.N / 2, 256);
   if (a.d == 2) g_kronsum_kernel<2><<<grid, 256, 0, stream>>>(a);
-  else if (a.d == 3) g_kronsum_kernel<3><<<grid, 256, 0, stream>>>(a);
+  else if (a.d == 3) g_kronsum_seq_kernel<3><<<grid, 256, 0, stream>>>(a);
   else return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
