@@ -1,0 +1,80 @@
+"""The paper's own server benchmarks on one B200: Table 5 (2-D Schnakenberg, T = 2, 6000 steps,
+N = 2 * 300^2 / 450^2 / 600^2) and Table 7 (3-D FitzHugh-Nagumo, T = 150,
+10000 steps, N = 2 * 100^3 / 150^3 / 200^3), exprk3ds_real and exprk3ds_cplx,
+fp64.  Wall-clock seconds of the whole integration (phi bank included, in brackets as in the
+paper) next to the paper's V100 "CUDA double" column.
+
+    python tools/paper_tables.py [--quick]  > profiles/paper_tables_r01.json
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+from paper_2310_07551_b200 import kx  # noqa: E402
+
+# (table, model, d, n, T, steps, scheme, paper V100 CUDA double seconds (phi seconds))
+ROWS = [
+    ("Table 5", "schnakenberg", 2, 300, 2.0, 6000, "etd3rkds", (7.32, 0.31)),
+    ("Table 5", "schnakenberg", 2, 450, 2.0, 6000, "etd3rkds", (16.39, 0.54)),
+    ("Table 5", "schnakenberg", 2, 600, 2.0, 6000, "etd3rkds", (26.15, 0.83)),
+    ("Table 5", "schnakenberg", 2, 300, 2.0, 6000, "exprk3ds_cplx", (16.33, 0.52)),
+    ("Table 5", "schnakenberg", 2, 450, 2.0, 6000, "exprk3ds_cplx", (46.28, 1.01)),
+    ("Table 5", "schnakenberg", 2, 600, 2.0, 6000, "exprk3ds_cplx", (89.93, 1.73)),
+    ("Table 7", "fhn", 3, 100, 150.0, 10000, "etd3rkds", (57.31, 0.28)),
+    ("Table 7", "fhn", 3, 150, 150.0, 10000, "etd3rkds", (251.62, 0.40)),
+    ("Table 7", "fhn", 3, 200, 150.0, 10000, "etd3rkds", (685.89, 0.44)),
+    ("Table 7", "fhn", 3, 100, 150.0, 10000, "exprk3ds_cplx", (127.47, 0.24)),
+    ("Table 7", "fhn", 3, 150, 150.0, 10000, "exprk3ds_cplx", (470.61, 0.33)),
+    ("Table 7", "fhn", 3, 200, 150.0, 10000, "exprk3ds_cplx", (1469.11, 0.45)),
+]
+
+
+def run(model, d, n, T, steps, scheme):
+    prob = inputs.make_problem(model, d, n, seed=0)
+    ctx = kx.Context(0)
+    ctx.set_grid(prob.n, 2)
+    for c in range(2):
+        for mu in range(d):
+            ctx.set_direction_matrix(c, mu + 1, prob.A[c][mu])
+    ctx.set_model(prob.model, prob.params)
+    U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx.set_tau(T / steps, scheme)
+    ctx.sync()
+    t_phi = time.perf_counter() - t0
+    ctx.step_n(U, steps)
+    ctx.sync()
+    total = time.perf_counter() - t0
+    finite = all(bool(torch.isfinite(u).all()) for u in U)
+    ctx.close()
+    return total, t_phi, finite
+
+
+def main():
+    quick = "--quick" in sys.argv
+    out = {"note": "wall-clock seconds of the whole integration on one B200 (phi bank in "
+                   "brackets, as the paper's tables); the paper's column is CUDA double on a "
+                   "V100 16 GB (context, other hardware)", "rows": []}
+    for table, model, d, n, T, steps, scheme, paper in ROWS:
+        if quick and steps * n ** d > 6000 * 450 ** 2:
+            continue
+        total, t_phi, finite = run(model, d, n, T, steps, scheme)
+        row = {"table": table, "model": model, "N": f"2*{n}^{d}", "T": T, "steps": steps,
+               "scheme": scheme, "seconds": round(total, 3), "phi_seconds": round(t_phi, 3),
+               "steps_per_s": round(steps / (total - t_phi), 1), "finite": finite,
+               "paper_v100_double_seconds": paper[0], "paper_phi_seconds": paper[1],
+               "speedup_vs_paper": round(paper[0] / total, 1)}
+        out["rows"].append(row)
+        print(json.dumps(row), file=sys.stderr, flush=True)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
