@@ -451,29 +451,46 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   // its empty-wait then targets a stage every warp left a whole k-tile ago (measured best of
   // k-step 0 / 4 / 12 / 28: +0.7% at C2)
   constexpr int PRODUCE_KK = BK - 4;
+  // ragged K (kseg not a multiple of BK, e.g. the paper's n = 100, 150, 200): the last k-tile
+  // of every segment runs only its valid k-steps (the zero-filled rows would add exact zeros)
+  const int kps = (p.kseg + BK - 1) / BK;
+  const int ktail = p.kseg - (kps - 1) * BK;   // valid k of a segment's last k-tile
+  int cks = ck % kps;                          // k-tile position inside its segment
+  auto kstep = [&](const double* as, const double* bs, int kk) {
+    double af[FM], bf[FN];
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
+      else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+    }
+#pragma unroll
+    for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  };
   while (true) {
     const int stage_c = ckt % STAGES;
     mbar_wait(full + stage_c, (ckt / STAGES) & 1);
     const double* as = As + stage_c * A_ST;
     const double* bs = Bs + stage_c * B_ST;
+    if (ktail == BK || cks != kps - 1) {
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[FM], bf[FN];
-#pragma unroll
-      for (int i = 0; i < FM; ++i) {
-        if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
-        else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+      for (int kk = 0; kk < BK; kk += 4) {
+        kstep(as, bs, kk);
+        if (kk == PRODUCE_KK) produce();
       }
+    } else {
 #pragma unroll
-      for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
-#pragma unroll
-      for (int i = 0; i < FM; ++i)
-#pragma unroll
-        for (int j = 0; j < FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-      if (kk == PRODUCE_KK) produce();
+      for (int kk = 0; kk < BK; kk += 4) {
+        if (kk < ktail) kstep(as, bs, kk);
+        if (kk == PRODUCE_KK) produce();
+      }
     }
     mbar_arrive(empty + stage_c);
     ++ckt;
+    if (++cks == kps) cks = 0;
     if (++ck < cs.ke) continue;
 
     // ---- segment finished
@@ -560,6 +577,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     }
     if (!cit.next(cs)) break;
     ck = cs.kb;
+    cks = ck % kps;
     cd = T_::coords(p, sc, cs.tl);
     T_::zero(acc);
   }
