@@ -235,8 +235,14 @@ struct GemmTile {
       for (int it = 0; it < IB; ++it) {
         const int c = tid + it * NT;
         const int kr = c / CPR_B, nc = (c % CPR_B) * VEC;
-        const bool v = cd.n0 + nc < p.N;
-        offB[it] = kr * ldb + (v ? cd.n0 + nc : 0);
+        const int np = cd.n0 + nc;
+        const bool v = np < p.N;
+        if (p.nflat) {   // flattened batches: column np is batch np / nflat
+          const int b = v ? np / p.nflat : 0;
+          offB[it] = v ? b * (int)p.sB_b + kr * ldb + (np - b * p.nflat) : kr * ldb;
+        } else {
+          offB[it] = kr * ldb + (v ? np : 0);
+        }
         okB |= (unsigned)v << it;
       }
       const int kps = (p.kseg + BK - 1) / BK;
@@ -296,7 +302,7 @@ struct GemmTile {
     if constexpr (VEC == 2) {
       // fast paths for whole interior tiles (every launch of the large configs): no bounds
       // checks, row pointers hoisted, the D loads issued before the stores
-      const bool plain = !PEER && mask == ~0u && !E && diag == 0.0 && cd.m0 + BM <= M &&
+      const bool plain = !PEER && !p.nflat && mask == ~0u && !E && diag == 0.0 && cd.m0 + BM <= M &&
                          cd.n0 + BN <= N;
       if (plain) {
         const long long ls = 8 * p.ldc;
@@ -334,31 +340,38 @@ struct GemmTile {
         const int n = cd.n0 + wn0 + j * 8 + 2 * t4;
         if (n >= N || !((mask >> (i * FN + j)) & 1u)) continue;
         double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+        // element offsets of (m, n) in C / D / E (flattened batches: n is batch n / nflat)
+        long long oc = (long long)m * p.ldc + n, od = (long long)m * p.ldd + n, oe = (long long)m * p.lde + n;
+        if (p.nflat) {
+          const int b = n / p.nflat, nn = n - b * p.nflat;
+          oc = b * p.sC_b + (long long)m * p.ldc + nn;
+          od = b * p.sD_b + (long long)m * p.ldd + nn;
+          oe = b * p.sE_b + (long long)m * p.lde + nn;
+        }
         if constexpr (VEC == 2) {
           if (D) {
-            const double2 d2 = *reinterpret_cast<const double2*>(D + (long long)m * p.ldd + n);
+            const double2 d2 = *reinterpret_cast<const double2*>(D + od);
             v0 += beta * d2.x;
             v1 += beta * d2.y;
           }
           if (E) {
-            const double2 e2 = *reinterpret_cast<const double2*>(E + (long long)m * p.lde + n);
+            const double2 e2 = *reinterpret_cast<const double2*>(E + oe);
             v0 += gamma * e2.x;
             v1 += gamma * e2.y;
           }
           if (m == n) v0 += diag;
           if (m == n + 1) v1 += diag;
-          *reinterpret_cast<double2*>(out_ptr(p, cd.s, C + (long long)m * p.ldc + n)) =
-              make_double2(v0, v1);
+          *reinterpret_cast<double2*>(out_ptr(p, cd.s, C + oc)) = make_double2(v0, v1);
         } else {
-          if (D) v0 += beta * D[(long long)m * p.ldd + n];
-          if (E) v0 += gamma * E[(long long)m * p.lde + n];
+          if (D) v0 += beta * D[od];
+          if (E) v0 += gamma * E[oe];
           if (m == n) v0 += diag;
-          *out_ptr(p, cd.s, C + (long long)m * p.ldc + n) = v0;
+          *out_ptr(p, cd.s, C + oc) = v0;
           if (n + 1 < N) {
-            if (D) v1 += beta * D[(long long)m * p.ldd + n + 1];
-            if (E) v1 += gamma * E[(long long)m * p.lde + n + 1];
+            if (D) v1 += beta * D[od + 1];
+            if (E) v1 += gamma * E[oe + 1];
             if (m == n + 1) v1 += diag;
-            *out_ptr(p, cd.s, C + (long long)m * p.ldc + n + 1) = v1;
+            *out_ptr(p, cd.s, C + oc + 1) = v1;
           }
         }
       }
@@ -727,7 +740,17 @@ double gemm_flops(const GemmArgs& g) {
   return 2.0 * g.M * (double)g.N * (double)g.kseg * g.nseg * g.ns * g.nt * g.nb;
 }
 
-cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream) {
+cudaError_t launch_gemm(const GemmArgs& g_in, cudaStream_t stream) {
+  GemmArgs g = g_in;
+  // batched COL-layout launches (middle modes) with ragged N: one launch over nb * N columns
+  // instead of nb launches' worth of padded tiles (the paper's n = 100, 150, 200)
+  g.nflat = 0;
+  if (!g.arow && g.nb > 1 && g.N % 64 != 0 && g.N % 2 == 0 && !g.peer.P &&
+      (long long)g.N * g.nb < (1LL << 30) && g.sB_b * (long long)g.nb < (1LL << 31)) {
+    g.nflat = g.N;
+    g.N *= g.nb;
+    g.nb = 1;
+  }
   const int nz = g.ns * g.nt * g.nb;
   if (g.M <= 0 || g.N <= 0 || nz <= 0) return cudaSuccess;
   if (g.kseg <= 0) return cudaErrorInvalidValue;

@@ -57,6 +57,10 @@ struct GemmArgs {
   double* sk_ws = nullptr;
   int* sk_flags = nullptr;
   PeerMap peer;                    // epilogue stores redirected to peers (P > 0)
+  // set by launch_gemm (not by callers): batched COL-layout launches whose N is not a multiple
+  // of the tile width are run as one launch over N' = nb N columns; column n' is batch
+  // n' / nflat, column n' % nflat (the B/C/D/E batch strides apply per column)
+  int nflat = 0;
 };
 constexpr int kSkSlots = 304;    // partial-tile slots of 128x128 doubles (>= 2 x SM count)
 constexpr int kSkFlags = 2048;   // counters: a pair per split tile
