@@ -53,7 +53,10 @@ NcclApi& nccl() {
 // the producing and the consuming phase (stream order in an in-process group, a one-double
 // NCCL all-reduce across processes).  Real schemes with the tridiagonal (halo) schedule.
 bool dist_banded(const kx_ctx* c);
-bool p2p_on(const kx_ctx* c) { return c->p2p && !c->cplx && dist_banded(c); }
+bool p2p_on(const kx_ctx* c) {
+  // peer_redirect works in 32-bit offsets: every redirected buffer (nslots x Nloc) must fit
+  return c->p2p && !c->cplx && dist_banded(c) && (long long)c->nslots * c->Nloc < (1LL << 31);
+}
 
 void p2p_close(kx_ctx* c) {
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);

@@ -31,12 +31,14 @@ struct PeerMap {
   const double* local_base[MAXS] = {};
   double* peer_base[MAXS][kMaxPeers] = {};
 };
+// 32-bit arithmetic: the host enables peer stores only when a buffer holds < 2^31 doubles
 __device__ __forceinline__ double* peer_redirect(const PeerMap& pm, int s, double* ptr) {
   if (pm.P == 0) return ptr;
-  const long long off = ptr - pm.local_base[s];
-  const long long slot = off / pm.span, within = off - slot * pm.span;
-  const long long q = within / pm.chunk;
-  return pm.peer_base[s][q] + slot * pm.span + pm.rank * pm.chunk + (within - q * pm.chunk);
+  const unsigned off = (unsigned)(ptr - pm.local_base[s]);
+  const unsigned span = (unsigned)pm.span, chunk = (unsigned)pm.chunk;
+  const unsigned slot = off / span, within = off - slot * span;
+  const unsigned q = within / chunk;
+  return pm.peer_base[s][q] + (size_t)slot * span + (size_t)pm.rank * chunk + (within - q * chunk);
 }
 
 struct GemmArgs {
