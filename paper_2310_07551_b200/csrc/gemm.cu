@@ -81,6 +81,9 @@ template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES
 struct Cfg {
   static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
   static constexpr int NT = WARPS_M * WARPS_N * 32;
+  // resident CTAs per SM the register budget must allow (512 threads: 1 at <= 128 registers;
+  // 256: 2 at <= 128; 128: 3 at <= 170)
+  static constexpr int MINB = NT >= 512 ? 1 : (NT >= 256 ? 2 : 3);
   static constexpr int SA = AROW ? (BK + 4) : (BM + 4);   // smem row stride (doubles)
   static constexpr int A_ST = AROW ? BM * SA : BK * SA;
   static constexpr int SB = BN + 4;
@@ -387,7 +390,8 @@ struct GemmTile {
 };
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
-__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT)
+__global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT,
+                                  Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::MINB)
     gemm_kernel(const GemmArgs p, const Sched sc) {
   using T_ = GemmTile<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
   using Coord = typename T_::Coord;
@@ -463,7 +467,9 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   // the prefetch of k-tile t+STAGES-1 is issued behind the DMMAs of this tile's last k-step:
   // its empty-wait then targets a stage every warp left a whole k-tile ago (measured best of
   // k-step 0 / 4 / 12 / 28: +0.7% at C2)
-  constexpr int PRODUCE_KK = BK - 4;
+  // with 2 stages the refill of the other stage must start at the first k-step (one k-tile
+  // of latency hiding); with 3 it is issued behind the last k-step
+  constexpr int PRODUCE_KK = STAGES == 2 ? 0 : BK - 4;
   // ragged K (kseg not a multiple of BK, e.g. the paper's n = 100, 150, 200): the last k-tile
   // of every segment runs only its valid k-steps (the zero-filled rows would add exact zeros)
   const int kps = (p.kseg + BK - 1) / BK;
