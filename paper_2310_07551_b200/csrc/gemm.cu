@@ -20,6 +20,8 @@
 // epilogue C = alpha*acc + beta*D + gamma*E + diag*I with 16-B stores.
 #include "kx_internal.h"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -113,6 +115,9 @@ struct Cfg {
 // CTAs are co-resident: cooperative launch).
 struct Sched {
   int tiles_m = 1, tiles_n = 1, m_fastest = 0, ktiles = 0;
+  // > 1: cluster split-K — the CTAs of one thread-block cluster (csplit of them) each take an
+  // equal k-range of the same tile and reduce their partials through distributed shared memory
+  int csplit = 0;
   int G = 1, G_sk = 0;
   long long dp_tiles = 0, sk_units = 0;
 };
@@ -513,7 +518,43 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     if (++ck < cs.ke) continue;
 
     // ---- segment finished
-    if (cs.kb == 0 && cs.ke == sc.ktiles) {
+    if (sc.csplit > 1) {
+      // cluster split-K: publish the partial in this CTA's (now idle) pipeline shared memory,
+      // then every CTA sums its share of the fragments over the cluster's partials in
+      // cluster-rank (= k) order, read through DSMEM, and stores that share
+      namespace cg = cooperative_groups;
+      cg::cluster_group cl = cg::this_cluster();
+      cp_async_wait<0>();
+      __syncthreads();
+      double* part = smem;
+#pragma unroll
+      for (int a = 0; a < FM; ++a)
+#pragma unroll
+        for (int c = 0; c < FN; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) part[((a * FN + c) * 2 + e) * NT + tid] = acc[a][c][e];
+      cl.sync();
+      const int q = (int)cl.block_rank(), S = sc.csplit;
+      unsigned mask = 0;
+#pragma unroll
+      for (int f = 0; f < FM * FN; ++f)
+        if (f % S == q) mask |= 1u << f;
+      T_::zero(acc);
+      for (int j = 0; j < S; ++j) {
+        const double* pj = cl.map_shared_rank(part, j);
+#pragma unroll
+        for (int a = 0; a < FM; ++a)
+#pragma unroll
+          for (int c = 0; c < FN; ++c)
+            if ((mask >> (a * FN + c)) & 1u) {
+#pragma unroll
+              for (int e = 0; e < 2; ++e) acc[a][c][e] += pj[((a * FN + c) * 2 + e) * NT + tid];
+            }
+      }
+      T_::epilogue(p, cd, acc, mask);
+      cl.sync();   // no CTA leaves while its partial may still be read
+      break;       // exactly one segment per CTA in this mode
+    } else if (cs.kb == 0 && cs.ke == sc.ktiles) {
       T_::epilogue(p, cd, acc, ~0u);
     } else {
       // split tile (stream-K): every contributor publishes its partial and counts itself in.
@@ -635,6 +676,39 @@ cudaError_t prepare_cfg() {
 }
 
 int num_sms();
+template <int BM, int WM>
+constexpr int FM_OF() { return WM / 8; }
+template <int BN, int WN>
+constexpr int FN_OF() { return WN / 8; }
+
+// clusters of S CTAs of this configuration that can be resident at once (GPC packing), cached
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER>
+int max_clusters(int S) {
+  static int cache[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  if (S < 1 || S > 8) return 0;
+  if (cache[S] < 0) {
+    using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(S * 64);
+    cfg.blockDim = dim3(C_::NT);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, &cfg) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    cache[S] = n;
+  }
+  return cache[S];
+}
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
@@ -651,10 +725,30 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
   const long long Gmax = (long long)num_sms() * P_::occ;
   sc.G = (int)std::min<long long>(T, Gmax);
   sc.dp_tiles = T;
+  // few tiles and a long K: split every tile over the CTAs of a cluster (DSMEM reduction)
+  {
+    static const int cs_env = [] {   // KX_GEMM_CSPLIT=0: tuning experiments only
+      const char* e = getenv("KX_GEMM_CSPLIT");
+      return e ? atoi(e) : 1;
+    }();
+    const int partial = FM_OF<BM, WM>() * FN_OF<BN, WN>() * 2 * C_::NT;   // doubles per partial
+    for (int S = 8; cs_env && S >= 2 && T * 4 <= Gmax; S /= 2) {
+      if (T * S <= Gmax && sc.ktiles % S == 0 && sc.ktiles / S >= 1 && g.kseg * g.nseg >= 128 &&
+          partial * 8 <= C_::SMEM && max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(S) >= T &&
+          T * S >= std::min<long long>(Gmax, T * sc.ktiles / 2)) {   // at least the stream-K split's CTAs
+        sc.csplit = S;
+        sc.G = (int)(T * S);
+        sc.dp_tiles = 0;
+        sc.sk_units = T * sc.ktiles;
+        sc.G_sk = (int)(T * S);
+        break;
+      }
+    }
+  }
   // stream-K needs two workspace slots per CTA and a counter pair per split tile
   const bool sk_ok = g.sk_ws && g.sk_flags && 2 * Gmax * BM * BN <= (long long)kSkSlots * 128 * 128 &&
                      sc.ktiles >= 2;
-  if (sk_ok && T % Gmax != 0) {
+  if (sk_ok && sc.csplit == 0 && T % Gmax != 0) {
     long long dp = (T / Gmax) * Gmax;
     if (dp >= Gmax && (T - dp) * 2 < Gmax) dp -= Gmax;   // short tail: spread one more wave
     // >= 4 k-tiles per CTA behind a data-parallel part, >= 2 when the whole launch is split
@@ -676,9 +770,26 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
   }
   static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only
   if (trace)
-    fprintf(stderr, "kx-gemm %s M=%d N=%d K=%dx%d nz=%d cfg=%dx%dx%d tiles=%lld kt=%d G=%d dp=%lld sk_units=%lld G_sk=%d flops=%.4g\n",
+    fprintf(stderr, "kx-gemm %s M=%d N=%d K=%dx%d nz=%d cfg=%dx%dx%d tiles=%lld kt=%d G=%d dp=%lld sk_units=%lld G_sk=%d csplit=%d (max clusters of 8/4/2: %d/%d/%d) flops=%.4g\n",
             AROW ? "row" : "col", g.M, g.N, g.kseg, g.nseg, nz, BM, BN, BK, T, sc.ktiles, sc.G,
-            sc.dp_tiles, sc.sk_units, sc.G_sk, 2.0 * g.M * g.N * (double)g.kseg * g.nseg * nz);
+            sc.dp_tiles, sc.sk_units, sc.G_sk, sc.csplit, max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(8),
+            max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(4), max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(2),
+            2.0 * g.M * g.N * (double)g.kseg * g.nseg * nz);
+  if (sc.csplit > 1) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sc.G);
+    cfg.blockDim = dim3(C_::NT);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = sc.csplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
+  }
   if (sc.sk_units > 0) {
     // stream-K CTAs wait on each other: a cooperative launch guarantees that the whole grid is
     // co-resident even when other kernels share the GPU (otherwise the driver refuses it)
