@@ -783,3 +783,25 @@ def test_fused_small_single_component_linear(kx, scheme):
     K = kronsum_assemble(A)
     exact = scipy.linalg.expm(steps * tau * K) @ u0
     assert relerr(out[True], exact) <= (1e-5 if scheme == "etd2rkds" else 1e-6)
+
+
+def test_new_entry_points_reject_bad_use(kx):
+    """Error paths of kx_step_n, kx_set_fused_small, kx_group_set_p2p and the IPC calls."""
+    prob = inputs.make_problem("schnakenberg", 2, [16, 16], seed=1)
+    c = kx.Context(0)
+    U = [dev(u) for u in prob.U0]
+    with pytest.raises(kx.KxError):          # no grid / no bank yet
+        c.step_n(U, 3)
+    setup_problem(c, prob, "etd3rkds", 1e-4)
+    with pytest.raises(kx.KxError):          # negative step count
+        c.step_n(U, -1)
+    with pytest.raises(kx.KxError):          # aliased components
+        c.step_n([U[0], U[0]], 1)
+    c.step_n(U, 0)                           # zero steps: a no-op
+    with pytest.raises(kx.KxError, match="NCCL"):   # IPC export needs an NCCL rank
+        c.ipc_export()
+    c.close()
+    grp = kx.Group(2)
+    with pytest.raises(kx.KxError):          # p2p before set_tau
+        grp.set_p2p(True)
+    grp.close()
