@@ -824,6 +824,11 @@ cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t str
 template <bool AROW, int VEC>
 void prepare_layout() {
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>();
+  for (int S = 2; S <= 8; S *= 2) {   // cluster residency queries outside any graph capture
+    max_clusters<128, 128, 32, 32, 32, AROW, VEC, 3, false>(S);
+    max_clusters<128, 64, 16, 32, 32, AROW, VEC, 3, false>(S);
+    max_clusters<64, 64, 16, 32, 32, AROW, VEC, 3, false>(S);
+  }
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>();
   prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>();
   prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>();
