@@ -733,9 +733,15 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
     }();
     const int partial = FM_OF<BM, WM>() * FN_OF<BN, WN>() * 2 * C_::NT;   // doubles per partial
     for (int S = 8; cs_env && S >= 2 && T * 4 <= Gmax; S /= 2) {
-      if (T * S <= Gmax && sc.ktiles % S == 0 && sc.ktiles / S >= 1 && g.kseg * g.nseg >= 128 &&
-          partial * 8 <= C_::SMEM && max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(S) >= T &&
-          T * S >= std::min<long long>(Gmax, T * sc.ktiles / 2)) {   // at least the stream-K split's CTAs
+      // (cluster boundaries are tile boundaries for any k-tile count: CTA i of the cluster of
+      // tile t starts at k-tile floor(i kt / S))
+      if (T * S <= Gmax && sc.ktiles >= S && g.kseg * g.nseg >= 128 && partial * 8 <= C_::SMEM &&
+          max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(S) >= T &&
+          // the 128x128 configuration keeps stream-K when that spreads over more CTAs (512^2:
+          // 128 vs 64 CTAs); the small-tile configurations (ragged / mid-size shapes such as the
+          // paper's 300^2), whose stream-K splits have many contributors per tile, take the
+          // cheaper DSMEM reduction (measured: 300^2 Tucker 45 -> 28 us)
+          (cs_env == 2 || BM * BN < 128 * 128 || T * S >= std::min<long long>(Gmax, T * sc.ktiles / 2))) {
         sc.csplit = S;
         sc.G = (int)(T * S);
         sc.dp_tiles = 0;
@@ -824,14 +830,15 @@ cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t str
 template <bool AROW, int VEC>
 void prepare_layout() {
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>();
-  for (int S = 2; S <= 8; S *= 2) {   // cluster residency queries outside any graph capture
+  prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>();
+  prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>();
+  prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>();
+  // cluster residency queries outside any graph capture, after the smem attributes are set
+  for (int S = 2; S <= 8; S *= 2) {
     max_clusters<128, 128, 32, 32, 32, AROW, VEC, 3, false>(S);
     max_clusters<128, 64, 16, 32, 32, AROW, VEC, 3, false>(S);
     max_clusters<64, 64, 16, 32, 32, AROW, VEC, 3, false>(S);
   }
-  prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>();
-  prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>();
-  prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>();
 }
 
 int num_sms() {

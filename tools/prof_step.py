@@ -22,6 +22,8 @@ ap.add_argument("--config", default="C2")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--eager", action="store_true")
 ap.add_argument("--tucker", nargs=2, type=int, default=None)
+ap.add_argument("--n", type=int, default=None, help="override the config's grid extent")
+ap.add_argument("--scheme", default=None)
 a = ap.parse_args()
 
 ctx = kx.Context(0)
@@ -39,7 +41,11 @@ if a.tucker:
     ctx.sync()
     torch.cuda.profiler.stop()
 else:
-    cfg = inputs.CONFIGS[a.config]
+    cfg = dict(inputs.CONFIGS[a.config])
+    if a.n:
+        cfg["n"] = a.n
+    if a.scheme:
+        cfg["scheme"] = a.scheme
     prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"])
     ctx.set_grid(prob.n, 2)
     for c in range(2):
