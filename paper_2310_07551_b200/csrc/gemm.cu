@@ -794,7 +794,15 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
+    const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
+    if (ce == cudaSuccess) return ce;
+    // the cluster launch was refused (e.g. SMs taken by concurrent work): plain data-parallel
+    cudaGetLastError();
+    sc.csplit = 0;
+    sc.G = (int)std::min<long long>(T, Gmax);
+    sc.dp_tiles = T;
+    sc.sk_units = 0;
+    sc.G_sk = 0;
   }
   if (sc.sk_units > 0) {
     // stream-K CTAs wait on each other: a cooperative launch guarantees that the whole grid is
