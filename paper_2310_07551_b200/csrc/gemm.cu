@@ -817,7 +817,14 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
+    const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
+    if (ce != cudaErrorCooperativeLaunchTooLarge) return ce;
+    // not all CTAs can be co-resident right now: the data-parallel schedule needs no waits
+    cudaGetLastError();
+    sc.G = (int)std::min<long long>(T, Gmax);
+    sc.dp_tiles = T;
+    sc.sk_units = 0;
+    sc.G_sk = 0;
   }
   gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc);
   return cudaGetLastError();
