@@ -265,12 +265,16 @@ def setup_ctx(kx, prob, scheme, tau, stream):
 
 def other_configs(kx, torch, stream, steps=10):
     """Secondary workloads reported beside the headline (same timing protocol, fewer steps):
-    C3 (3D FitzHugh-Nagumo 128^3, exprk3ds_real) and the complex split on C2."""
+    C3 (3D FitzHugh-Nagumo 128^3, exprk3ds_real), the complex split on C2, and C4 (512^3 on
+    this one GPU, 3 timed steps)."""
     import inputs
     out = {}
     flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+    full_steps = steps
     for name, cfg_name, scheme in [("C3_fhn_128^3_etd3rkds_real", "C3", None),
-                                   ("C2_schnakenberg_1024^2_exprk3ds_cplx", "C2", "exprk3ds_cplx")]:
+                                   ("C2_schnakenberg_1024^2_exprk3ds_cplx", "C2", "exprk3ds_cplx"),
+                                   ("C4_fhn_512^3_etd3rkds_real_1gpu", "C4", None)]:
+        steps = 3 if cfg_name == "C4" else full_steps
         cfg = config_dict(cfg_name)
         if scheme:
             cfg["scheme"] = scheme
