@@ -832,9 +832,15 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
 
 template <bool AROW, int VEC>
 cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
-  // direct peer stores (sharded steps, large shapes): the 128 x 128 configuration only, in its
-  // own instantiation so the redirect arithmetic costs the plain kernels no registers
-  if (g.peer.P) return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
+  // direct peer stores (sharded steps): separate instantiations so the redirect arithmetic
+  // costs the plain kernels no registers
+  if (g.peer.P) {
+    switch (which) {
+      case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
+      case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
+      default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
+    }
+  }
   switch (which) {
     case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>(g, nz, stream);
     case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
@@ -846,6 +852,8 @@ template <bool AROW, int VEC>
 void prepare_layout() {
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>();
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>();
+  prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, true>();
+  prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, true>();
   prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>();
   prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>();
   // cluster residency queries outside any graph capture, after the smem attributes are set
