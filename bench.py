@@ -496,6 +496,47 @@ def run_kx(args, rank, world, sharded):
     return res, cfg, prob
 
 
+def sharded_subrun(args, rank, world, timeout_s=420):
+    """N > 1 replicas runs also measure the north_star's multi-GPU workload: C4 (512^3)
+    slab-sharded over the same GPUs (direct peer stores + NCCL barriers), in child processes
+    with their own rendezvous and a timeout, so that a failure there cannot take the headline
+    line down.  Every rank joins; rank 0 returns the child's result (or the error)."""
+    import socket
+    import subprocess
+    import torch
+    import torch.distributed as dist
+    port = [None]
+    if rank == 0:
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port[0] = sk.getsockname()[1]
+        sk.close()
+    dist.broadcast_object_list(port, src=0)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+               MASTER_PORT=str(port[0]), LOCAL_RANK=os.environ.get("LOCAL_RANK", str(rank)))
+    cmd = [sys.executable, os.path.abspath(__file__), "--gpus", str(world), "--config", "C4",
+           "--mode", "sharded", "--steps", "5", "--warmup", "3", "--no-extras"]
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout_s)
+        out = {"rc": r.returncode}
+        if rank == 0:
+            lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+            if r.returncode == 0 and lines:
+                d = json.loads(lines[-1])
+                out = {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+                       "n_gpus": d["n_gpus"], "scaling": d["scaling"],
+                       "workload": d["config"]["workload"], "parallelism": d["config"]["parallelism"],
+                       "roofline_frac": d["roofline"]["frac"], "clocks": d.get("clocks")}
+            else:
+                out["error"] = (r.stderr.strip().splitlines() or ["no output"])[-1][:300]
+    except subprocess.TimeoutExpired:
+        out = {"error": f"timeout after {timeout_s} s"}
+    dist.barrier()
+    return out if rank == 0 else None
+
+
 def main():
     global SCHEME_OVERRIDE
     args = parse()
@@ -541,6 +582,9 @@ def main():
         dist.init_process_group("nccl")
     sharded = args.mode == "sharded" or (world > 1 and args.mode == "auto" and cfg["d"] == 3)
     res, cfg, prob = run_kx(args, rank, world, sharded)
+    extra_sharded = None
+    if world > 1 and not sharded and not args.no_extras and args.mode == "auto":
+        extra_sharded = sharded_subrun(args, rank, world)
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -601,6 +645,8 @@ def main():
         v1, _, sample1 = oracle_sample(args.config, args.cpu_seconds / 2, threads=1)
         line["cpu_baseline_1core"] = {"value": v1, "unit": "steps/s", "cores": 1, "kind": "oracle",
                                       "sample": sample1}
+    if extra_sharded is not None:
+        line["sharded_c4"] = extra_sharded
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
