@@ -805,3 +805,35 @@ def test_new_entry_points_reject_bad_use(kx):
     with pytest.raises(kx.KxError):          # p2p before set_tau
         grp.set_p2p(True)
     grp.close()
+
+
+def test_fused_small_integrate_host_watchdog_profile(kx):
+    """The small-grid kernel through the other entry points: kx_integrate_host (all steps in
+    one launch) equals kx_step on the device; with the NaN watchdog on, kx_step_n falls back
+    to per-step launches and stays silent on a healthy run; profiling records the fused kernel
+    as a mode-product launch."""
+    prob = inputs.make_problem("fhn", 2, [40, 32], seed=4)
+    tau, steps = 0.01, 7
+    c = kx.Context(0)
+    setup_problem(c, prob, "etd3rkds", tau)
+    Uh = [np.ascontiguousarray(u.copy()) for u in prob.U0]
+    c.integrate_host(Uh, steps)
+    U = [dev(u) for u in prob.U0]
+    for _ in range(steps):
+        c.step(U)
+    c.sync()
+    for k in range(2):
+        assert np.array_equal(Uh[k], U[k].cpu().numpy())
+    c.set_nan_check(True)
+    c.reset_counters()
+    c.step_n(U, 3)
+    c.sync()
+    assert c.counters()["gemm_launches"] == 3     # one fused launch per step
+    c.set_nan_check(False)
+    c.set_profiling(True)
+    c.step(U)
+    c.sync()
+    prof = c.profile()
+    c.set_profiling(False)
+    assert prof["gemm_launches"] >= 1 and prof["gemm_flops"] > 0
+    c.close()
