@@ -7,6 +7,8 @@
 //   Schnakenberg: g1 = rho (a_u - u + u^2 v),  g2 = rho (a_v - u^2 v)
 //   FitzHugh-Nagumo: g1 = rho (-u (u^2 - 1) - v),  g2 = rho a1 (u - a2 v)
 #include "kx_internal.h"
+
+#include <algorithm>
 #include "kx_model.cuh"
 
 namespace kx {
@@ -412,7 +414,7 @@ int grid_for(long long work, int block) {
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
   }
   long long blocks = (work + block - 1) / block;
-  const long long cap = (long long)nsm * 8;   // 8 resident 256-thread CTAs per SM
+  const long long cap = (long long)nsm * 16;   // 2 waves of 8 resident 256-thread CTAs per SM
   if (blocks > cap) blocks = cap;
   return (int)(blocks < 1 ? 1 : blocks);
 }
@@ -440,7 +442,8 @@ cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t s
 
 cudaError_t launch_g_kronsum(const GKronArgs& a, cudaStream_t stream) {
   if (a.N <= 0) return cudaSuccess;
-  const int grid = grid_for(a.N / 2, 256);
+  // one wave of 8 CTAs per SM (its neighbour loads hit L2 better than two waves)
+  const int grid = (int)std::min<long long>(grid_for(a.N / 2, 256), 8LL * (grid_for(1LL << 40, 256) / 16));
   if (a.d == 2) g_kronsum_kernel<2><<<grid, 256, 0, stream>>>(a);
   else if (a.d == 3) g_kronsum_seq_kernel<3><<<grid, 256, 0, stream>>>(a);
   else return cudaErrorInvalidValue;
