@@ -496,7 +496,7 @@ def run_kx(args, rank, world, sharded):
     return res, cfg, prob
 
 
-def sharded_subrun(args, rank, world, timeout_s=420):
+def sharded_subrun(args, rank, world, timeout_s=240):
     """N > 1 replicas runs also measure the north_star's multi-GPU workload: C4 (512^3)
     slab-sharded over the same GPUs (direct peer stores + NCCL barriers), in child processes
     with their own rendezvous and a timeout, so that a failure there cannot take the headline
