@@ -308,6 +308,26 @@ def other_configs(kx, torch, stream, steps=10):
         ctx.close()
         del U
         torch.cuda.empty_cache()
+    # C1 with many steps per launch (kx_step_n: the small-grid cluster kernel keeps the state in
+    # shared memory across steps; one launch, so no L2 flush between its steps)
+    cfg = config_dict("C1")
+    prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
+    ctx, _ = setup_ctx(kx, prob, cfg["scheme"], cfg["T"] / cfg["m"], stream)
+    U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
+    nsteps = 3000   # the C1 protocol (T = 0.25, m = 3000) in one launch
+    ctx.step_n(U, 10)
+    ctx.sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record()
+        ctx.step_n(U, nsteps)
+        e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / nsteps
+    out["C1_schnakenberg_64^2_etd2rkds_step_n"] = {"steps_per_s": round(1e3 / ms, 1),
+                                                   "us_per_step": round(ms * 1e3, 2),
+                                                   "launches": 1, "steps_per_launch": nsteps}
+    ctx.close()
     return out
 
 
