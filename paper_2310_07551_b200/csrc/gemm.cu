@@ -710,70 +710,87 @@ int max_clusters(int S) {
   return cache[S];
 }
 
+// Schedule of one launch for one tile configuration (data-parallel waves, a stream-K tail or a
+// whole-launch split, or a cluster split-K) and its estimated time in microseconds: per SM,
+// the k-tiles it computes times the SM-alone k-tile time (4.2 us for 128x128x32 at full DMMA
+// rate, scaled by tile volume and the configuration's measured efficiency), plus ~3 us for a
+// global stream-K fix-up or ~0.5 us for a DSMEM one.
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER>
+double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
+  using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
+  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
+  prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
+  sc = Sched{};
+  sc.tiles_m = (g.M + BM - 1) / BM;
+  sc.tiles_n = (g.N + BN - 1) / BN;
+  sc.m_fastest = AROW ? 0 : 1;
+  sc.ktiles = ((g.kseg + BK - 1) / BK) * g.nseg;
+  const int nsm = num_sms();
+  const long long T = (long long)sc.tiles_m * sc.tiles_n * nz;
+  const long long Gmax = (long long)nsm * P_::occ;
+  const double kt_us = 4.2 * (BM * BN * BK) / (128.0 * 128 * 32) / eff;
+  const long long kt = sc.ktiles;
+  auto per_sm = [&](long long ctas, long long units_per_cta) {   // SM-alone k-tile units
+    return (double)((ctas + nsm - 1) / nsm) * (double)units_per_cta;
+  };
+  sc.G = (int)std::min<long long>(T, Gmax);
+  sc.dp_tiles = T;
+  double best = per_sm(T, kt) * kt_us;   // data-parallel
+  // cluster split-K (few tiles): every tile over the S CTAs of a cluster, DSMEM reduction
+  static const int cs_env = [] {   // KX_GEMM_CSPLIT=0: tuning experiments only
+    const char* e = getenv("KX_GEMM_CSPLIT");
+    return e ? atoi(e) : 1;
+  }();
+  const int partial = FM_OF<BM, WM>() * FN_OF<BN, WN>() * 2 * C_::NT;   // doubles per partial
+  for (int S = 8; cs_env && S >= 2 && T * 2 <= Gmax; S /= 2) {
+    if (T * S <= Gmax && kt >= S && (long long)g.kseg * g.nseg >= 128 && partial * 8 <= C_::SMEM &&
+        max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(S) >= T) {
+      const double t = per_sm(T * S, (kt + S - 1) / S) * kt_us + 0.5;
+      if (t < best) {
+        best = t;
+        sc.csplit = S;
+        sc.G = (int)(T * S);
+        sc.dp_tiles = 0;
+        sc.sk_units = T * kt;
+        sc.G_sk = (int)(T * S);
+      }
+    }
+  }
+  // stream-K (needs two workspace slots per CTA and a counter pair per split tile)
+  const bool sk_ok = g.sk_ws && g.sk_flags && 2 * Gmax * BM * BN <= (long long)kSkSlots * 128 * 128 &&
+                     kt >= 2 && T % Gmax != 0;
+  if (sk_ok) {
+    long long dp = (T / Gmax) * Gmax;
+    if (dp >= Gmax && (T - dp) * 2 < Gmax) dp -= Gmax;   // short tail: spread one more wave
+    // >= 4 k-tiles per CTA behind a data-parallel part, >= 2 when the whole launch is split
+    const long long units = (T - dp) * kt;
+    const int G_sk = (int)std::min<long long>(Gmax, units / (dp > 0 ? 4 : 2));
+    const bool worth = dp > 0 || (long long)g.kseg * g.nseg >= 128;   // tiny K: latency-bound
+    if (worth && G_sk >= 1 && 2 * (T - dp) <= kSkFlags) {
+      const double t = (per_sm(dp, kt) + per_sm(G_sk, (units + G_sk - 1) / G_sk)) * kt_us + 3.0;
+      if (t < 0.97 * best) {
+        best = t;
+        sc.csplit = 0;
+        sc.G = dp > 0 ? (int)Gmax : G_sk;
+        sc.dp_tiles = dp;
+        sc.sk_units = units;
+        sc.G_sk = G_sk;
+      }
+    }
+  }
+  return best;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
-cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
+cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t stream) {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
   cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
   if (e != cudaSuccess) return e;
   Sched sc;
-  sc.tiles_m = (g.M + BM - 1) / BM;
-  sc.tiles_n = (g.N + BN - 1) / BN;
-  sc.m_fastest = AROW ? 0 : 1;
-  sc.ktiles = ((g.kseg + BK - 1) / BK) * g.nseg;
+  plan_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(g, nz, eff, sc);
   const long long T = (long long)sc.tiles_m * sc.tiles_n * nz;
   const long long Gmax = (long long)num_sms() * P_::occ;
-  sc.G = (int)std::min<long long>(T, Gmax);
-  sc.dp_tiles = T;
-  // few tiles and a long K: split every tile over the CTAs of a cluster (DSMEM reduction)
-  {
-    static const int cs_env = [] {   // KX_GEMM_CSPLIT=0: tuning experiments only
-      const char* e = getenv("KX_GEMM_CSPLIT");
-      return e ? atoi(e) : 1;
-    }();
-    const int partial = FM_OF<BM, WM>() * FN_OF<BN, WN>() * 2 * C_::NT;   // doubles per partial
-    for (int S = 8; cs_env && S >= 2 && T * 4 <= Gmax; S /= 2) {
-      // (cluster boundaries are tile boundaries for any k-tile count: CTA i of the cluster of
-      // tile t starts at k-tile floor(i kt / S))
-      if (T * S <= Gmax && sc.ktiles >= S && g.kseg * g.nseg >= 128 && partial * 8 <= C_::SMEM &&
-          max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(S) >= T &&
-          // the 128x128 configuration keeps stream-K when that spreads over more CTAs (512^2:
-          // 128 vs 64 CTAs); the small-tile configurations (ragged / mid-size shapes such as the
-          // paper's 300^2), whose stream-K splits have many contributors per tile, take the
-          // cheaper DSMEM reduction (measured: 300^2 Tucker 45 -> 28 us)
-          (cs_env == 2 || BM * BN < 128 * 128 || T * S >= std::min<long long>(Gmax, T * sc.ktiles / 2))) {
-        sc.csplit = S;
-        sc.G = (int)(T * S);
-        sc.dp_tiles = 0;
-        sc.sk_units = T * sc.ktiles;
-        sc.G_sk = (int)(T * S);
-        break;
-      }
-    }
-  }
-  // stream-K needs two workspace slots per CTA and a counter pair per split tile
-  const bool sk_ok = g.sk_ws && g.sk_flags && 2 * Gmax * BM * BN <= (long long)kSkSlots * 128 * 128 &&
-                     sc.ktiles >= 2;
-  if (sk_ok && sc.csplit == 0 && T % Gmax != 0) {
-    long long dp = (T / Gmax) * Gmax;
-    if (dp >= Gmax && (T - dp) * 2 < Gmax) dp -= Gmax;   // short tail: spread one more wave
-    // >= 4 k-tiles per CTA behind a data-parallel part, >= 2 when the whole launch is split
-    const long long units = (T - dp) * sc.ktiles;
-    const int G_sk = (int)std::min<long long>(Gmax, units / (dp > 0 ? 4 : 2));
-    // time model in k-tile units: the split costs its fix-up (~3 us: partial store, fence,
-    // counter, partial loads) on top of the longest k-range
-    const double kt_us = 4.2 * (BM * BN * BK) / (128.0 * 128 * 32) * P_::occ;
-    const double classic = std::ceil((double)T / Gmax) * sc.ktiles;
-    const double split = (double)(dp / Gmax) * sc.ktiles +
-                         std::ceil((double)units / std::max(G_sk, 1)) + 3.0 / kt_us;
-    const bool worth = dp > 0 || (long long)g.kseg * g.nseg >= 128;   // tiny K: latency-bound
-    if (worth && G_sk >= 1 && 2 * (T - dp) <= kSkFlags && split < 0.97 * classic) {
-      sc.G = dp > 0 ? (int)Gmax : G_sk;
-      sc.dp_tiles = dp;
-      sc.sk_units = units;
-      sc.G_sk = G_sk;
-    }
-  }
   static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only
   if (trace)
     fprintf(stderr, "kx-gemm %s M=%d N=%d K=%dx%d nz=%d cfg=%dx%dx%d tiles=%lld kt=%d G=%d dp=%lld sk_units=%lld G_sk=%d csplit=%d (max clusters of 8/4/2: %d/%d/%d) flops=%.4g\n",
@@ -830,22 +847,30 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Pick the tile configuration with the smallest planned time (unless forced) and launch it.
+template <bool AROW, int VEC, bool PEER>
+cudaError_t launch_layout_p(const GemmArgs& g, int nz, int forced, const double* eff, cudaStream_t stream) {
+  Sched sc;
+  const double t0 = plan_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[0], sc);
+  const double t1 = plan_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[1], sc);
+  const double t2 = plan_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[2], sc);
+  int which = 0;
+  if (t1 < t0 * 0.999 && t1 <= t2) which = 1;
+  else if (t2 < t0 * 0.999 && t2 < t1) which = 2;
+  if (forced >= 0 && forced < 3) which = forced;
+  switch (which) {
+    case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[0], stream);
+    case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[1], stream);
+    default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[2], stream);
+  }
+}
+
 template <bool AROW, int VEC>
-cudaError_t launch_layout(const GemmArgs& g, int nz, int which, cudaStream_t stream) {
+cudaError_t launch_layout(const GemmArgs& g, int nz, int forced, const double* eff, cudaStream_t stream) {
   // direct peer stores (sharded steps): separate instantiations so the redirect arithmetic
   // costs the plain kernels no registers
-  if (g.peer.P) {
-    switch (which) {
-      case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
-      case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
-      default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, true>(g, nz, stream);
-    }
-  }
-  switch (which) {
-    case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>(g, nz, stream);
-    case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
-    default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3>(g, nz, stream);
-  }
+  if (g.peer.P) return launch_layout_p<AROW, VEC, true>(g, nz, forced, eff, stream);
+  return launch_layout_p<AROW, VEC, false>(g, nz, forced, eff, stream);
 }
 
 template <bool AROW, int VEC>
@@ -920,36 +945,19 @@ cudaError_t launch_gemm(const GemmArgs& g_in, cudaStream_t stream) {
     if (g.D[s]) vec = vec && aligned16(g.D[s]);
     if (g.E[s]) vec = vec && aligned16(g.E[s]);
   }
-  // Tile choice: minimise (waves x per-wave work) / efficiency on the SM count.  With the
-  // stream-K tail (k-tiles >= 8) a partial last wave costs only its fraction (+3% fix-up).
-  const int nsm = num_sms();
+  // Tile choice: the configuration whose planned schedule (plan_cfg) is fastest.
   static const TileChoice* tiles = [] {   // KX_GEMM_EFF="e0,e1,e2": tuning experiments only
     static TileChoice t[3] = {kTiles[0], kTiles[1], kTiles[2]};
     if (const char* e = getenv("KX_GEMM_EFF")) sscanf(e, "%lf,%lf,%lf", &t[0].eff, &t[1].eff, &t[2].eff);
     return t;
   }();
-  int best = 0;
-  double best_cost = 1e300;
-  for (int i = 0; i < 3; ++i) {
-    const TileChoice& c = tiles[i];
-    const double tiles = (double)((g.M + c.bm - 1) / c.bm) * ((g.N + c.bn - 1) / c.bn) * nz;
-    const double slots = (double)nsm * c.occ;
-    double waves = std::ceil(tiles / slots);
-    const int kt = (g.kseg + c.bk - 1) / c.bk * g.nseg;
-    if (kt >= 8 && waves / (tiles / slots) > 1.06) waves = 1.03 * tiles / slots;
-    const double cost = waves * c.occ * c.bm * c.bn / c.eff;
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
-      best = i;
-    }
-  }
+  const double eff[3] = {tiles[0].eff, tiles[1].eff, tiles[2].eff};
   static int forced = [] {
     const char* e = getenv("KX_GEMM_CFG");   // tuning experiments only: 0, 1, 2
     return e ? atoi(e) : -1;
   }();
-  if (forced >= 0 && forced < 3) best = forced;
-  if (g.arow) return vec ? launch_layout<true, 2>(g, nz, best, stream) : launch_layout<true, 1>(g, nz, best, stream);
-  return vec ? launch_layout<false, 2>(g, nz, best, stream) : launch_layout<false, 1>(g, nz, best, stream);
+  if (g.arow) return vec ? launch_layout<true, 2>(g, nz, forced, eff, stream) : launch_layout<true, 1>(g, nz, forced, eff, stream);
+  return vec ? launch_layout<false, 2>(g, nz, forced, eff, stream) : launch_layout<false, 1>(g, nz, forced, eff, stream);
 }
 
 }  // namespace kx
