@@ -729,6 +729,11 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
   const long long T = (long long)sc.tiles_m * sc.tiles_n * nz;
   const long long Gmax = (long long)nsm * P_::occ;
   const double kt_us = 4.2 * (BM * BN * BK) / (128.0 * 128 * 32) / eff;
+  static const double* fix = [] {   // KX_GEMM_FIX="sk_us,cluster_us": tuning experiments only
+    static double f[2] = {6.0, 0.5};   // tuned on the size sweep, the Tucker sweep and C2/C3
+    if (const char* e = getenv("KX_GEMM_FIX")) sscanf(e, "%lf,%lf", &f[0], &f[1]);
+    return f;
+  }();
   const long long kt = sc.ktiles;
   auto per_sm = [&](long long ctas, long long units_per_cta) {   // SM-alone k-tile units
     return (double)((ctas + nsm - 1) / nsm) * (double)units_per_cta;
@@ -745,7 +750,7 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
   for (int S = 8; cs_env && S >= 2 && T * 2 <= Gmax; S /= 2) {
     if (T * S <= Gmax && kt >= S && (long long)g.kseg * g.nseg >= 128 && partial * 8 <= C_::SMEM &&
         max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(S) >= T) {
-      const double t = per_sm(T * S, (kt + S - 1) / S) * kt_us + 0.5;
+      const double t = per_sm(T * S, (kt + S - 1) / S) * kt_us + fix[1];
       if (t < best) {
         best = t;
         sc.csplit = S;
@@ -767,7 +772,7 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
     const int G_sk = (int)std::min<long long>(Gmax, units / (dp > 0 ? 4 : 2));
     const bool worth = dp > 0 || (long long)g.kseg * g.nseg >= 128;   // tiny K: latency-bound
     if (worth && G_sk >= 1 && 2 * (T - dp) <= kSkFlags) {
-      const double t = (per_sm(dp, kt) + per_sm(G_sk, (units + G_sk - 1) / G_sk)) * kt_us + 3.0;
+      const double t = (per_sm(dp, kt) + per_sm(G_sk, (units + G_sk - 1) / G_sk)) * kt_us + fix[0];
       if (t < 0.97 * best) {
         best = t;
         sc.csplit = 0;
