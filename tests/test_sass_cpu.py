@@ -70,3 +70,13 @@ def test_small_grid_kernels_use_clusters_and_dmma(sass):
 
 def test_no_half_precision_mma_anywhere(sass):
     assert "HMMA" not in sass and not re.search(r"UTC\w*MMA", sass)
+
+
+def test_peer_store_gemms_fence_at_system_scope(sass):
+    """The GEMM instantiations that store straight into other ranks' buffers (the fused
+    all-to-all) end with a system-scope fence; the plain ones do not pay for it."""
+    peer = _functions(sass, r"gemm_kernel.*Li3ELb1E")     # ..., STAGES = 3, PEER = true
+    plain = _functions(sass, r"gemm_kernel.*Li3ELb0E")
+    assert len(peer) >= 6 and len(plain) >= 6
+    assert all("MEMBAR.SC.SYS" in f for f in peer)
+    assert not any("MEMBAR.SC.SYS" in f for f in plain)
