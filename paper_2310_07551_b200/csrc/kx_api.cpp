@@ -81,6 +81,7 @@ void kx_destroy(kx_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->watch) cudaFree(c->watch);
+  if (c->bar_buf) cudaFree(c->bar_buf);
   if (c->sk_ws) cudaFree(c->sk_ws);
   if (c->sk_flags) cudaFree(c->sk_flags);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
