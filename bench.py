@@ -209,14 +209,38 @@ def oracle_sample(cfg_name, seconds, threads=None):
 
 
 # -------------------------------------------------------------------------------- GPU arm --
+_PEAK = None
+
+
 def load_peak():
-    p = os.path.join(ROOT, "profiles", "peaks_r01.json")
+    """(fp64 DMMA TFLOP/s sustained, HBM copy GB/s, source) — measured IN THIS JOB by the
+    tools/peaks.cu microbenchmark (build/peaks: a 1.5 s sustained mma.sync.m8n8k4.f64 loop on
+    every SM, DFMA and copy loops; ~5 s), else the round-1 measurement on this pool.
+    MEASURED_PEAKS.json has no fp64 entry."""
+    global _PEAK
+    if _PEAK is not None:
+        return _PEAK
+    exe = os.path.join(ROOT, "build", "peaks")
+    if os.path.exists(exe):
+        try:
+            r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+            j = json.loads(r.stdout.strip().splitlines()[-1])
+            _PEAK = (float(j["dmma_tflops_sustained"]), float(j["hbm_copy_gbs"]),
+                     "measured in this job before the timed region: tools/peaks.cu (build/peaks), "
+                     f"fp64 DMMA mma.sync.m8n8k4 on all {j.get('sms')} SMs, "
+                     f"{j.get('dmma_sustained_ms', 0):.0f} ms sustained; MEASURED_PEAKS.json has no fp64 entry "
+                     "(bf16 sustained x nominal 45/2250 would give 28.0)")
+            return _PEAK
+        except Exception:
+            pass
     try:
-        with open(p) as f:
+        with open(os.path.join(ROOT, "profiles", "peaks_r01.json")) as f:
             j = json.load(f)
-        return float(j["dmma_tflops_sustained"]), float(j.get("hbm_copy_gbs", 0))
+        _PEAK = (float(j["dmma_tflops_sustained"]), float(j.get("hbm_copy_gbs", 0)),
+                 "profiles/peaks_r01.json (tools/peaks.cu on this pool, round 1): fp64 DMMA 1.5 s sustained")
     except Exception:
-        return None, None
+        _PEAK = (None, None, "unavailable")
+    return _PEAK
 
 
 def hbm_peak():
@@ -225,8 +249,8 @@ def hbm_peak():
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"
     except Exception:
-        _, h = load_peak()
-        return h, "profiles/peaks_r01.json hbm_copy_gbs"
+        _, h, _src = load_peak()
+        return h, "tools/peaks.cu copy kernel (this job)"
 
 
 def elementwise_roofline(prof):
@@ -332,13 +356,46 @@ def other_configs(kx, torch, stream, steps=10):
     return out
 
 
-def tucker_sweep(kx, torch, stream, budget_s=40.0):
-    """Tucker microbenchmark: one Tucker operator T(X, {L_mu}) on an n^d
-    fp64 tensor, dense flops 2 N d n / device time.  R back-to-back Tuckers are captured in a
-    CUDA graph and replayed between CUDA events (no host launch overhead in the number); the
-    tensors of the larger sizes exceed L2, the small ones are L2-resident by nature."""
-    import inputs  # noqa: F401
-    out = {}
+def _graph_time(torch, stream, fn, reps):
+    """Best-of-3 device ms per call of fn(), R back-to-back calls captured in a CUDA graph."""
+    for _ in range(2):
+        fn()
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    stream.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(3):
+        with torch.cuda.stream(stream):
+            e0.record()
+            g.replay()
+            e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        best = ms if best is None else min(best, ms)
+    del g
+    return best
+
+
+# batch sizes of the batched sweep: >= ~4 GFLOP per batched Tucker where memory allows
+BATCH = {(2, 64): 4096, (2, 128): 512, (2, 256): 64, (2, 512): 16, (2, 1024): 4,
+         (3, 64): 32, (3, 128): 4, (3, 256): 1}
+
+
+def tucker_sweep(kx, torch, stream, budget_s=60.0):
+    """Tucker microbenchmark, fp64, dense flops 2 N d n / device time:
+      * single: ONE Tucker operator T(X, {L_mu}) on an n^d tensor (its latency);
+      * batched: kx_tucker_batched over B independent n^d tensors sharing {L_mu} (throughput:
+        one GEMM launch per mode for the whole batch).
+    R back-to-back calls are captured in a CUDA graph and replayed between CUDA events (no host
+    launch overhead in the number); the larger working sets exceed L2, the small ones are
+    L2-resident by nature."""
+    single, batched, single_us, batch_of = {}, {}, {}, {}
     t_start = time.perf_counter()
     sizes = [(2, n) for n in (64, 128, 256, 512, 1024, 2048, 4096)] + \
             [(3, n) for n in (64, 128, 256, 512, 1024)]
@@ -347,60 +404,52 @@ def tucker_sweep(kx, torch, stream, budget_s=40.0):
             break
         N = n ** d
         fl = 2.0 * N * n * d
-        reps = int(min(200, max(3, 2e10 / fl)))
         ctx = kx.Context(stream.device.index, stream)
         ctx.set_grid([n] * d, 1)
-        X = torch.rand(N, dtype=torch.float64, device="cuda")
-        Y = torch.empty_like(X)
         L = torch.rand(n * n, dtype=torch.float64, device="cuda") / n
         Ls = [L] * d
-        for _ in range(2):
-            ctx.tucker(X, Y, Ls)
-        ctx.sync()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream, capture_error_mode="relaxed"):
-            for _ in range(reps):
-                ctx.tucker(X, Y, Ls)
-        g.replay()
-        stream.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        best = None
-        for _ in range(3):
-            with torch.cuda.stream(stream):
-                e0.record()
-                g.replay()
-                e1.record()
-            e1.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            best = ms if best is None else min(best, ms)
-        out[f"d{d}_n{n}"] = round(fl / best / 1e9, 2)
-        del g
+        B = BATCH.get((d, n), 0)
+        X = torch.rand(N * max(B, 1), dtype=torch.float64, device="cuda")
+        Y = torch.empty_like(X)
+        reps = int(min(200, max(3, 2e10 / fl)))
+        ms = _graph_time(torch, stream, lambda: ctx.tucker(X[:N], Y[:N], Ls), reps)
+        key = f"d{d}_n{n}"
+        single[key] = round(fl / ms / 1e9, 2)
+        single_us[key] = round(ms * 1e3, 2)
+        if B > 1:
+            reps = int(min(100, max(3, 2e10 / (fl * B))))
+            ms = _graph_time(torch, stream, lambda: ctx.tucker_batched(X, Y, Ls, B), reps)
+            batched[key] = round(fl * B / ms / 1e9, 2)
+            batch_of[key] = B
         ctx.close()
         del X, Y, L
         torch.cuda.empty_cache()
-    return out
+    return {"single": single, "single_us": single_us, "batched": batched, "batch": batch_of}
 
 
-def emulate_sharded_p8(kx, torch, stream, c4_one, P=8, steps=3):
+def emulate_sharded_p8(kx, torch, stream, c4_one, P=8, steps=3, warm=2):
     """The 8-GPU slab-sharded C4 step emulated on this one GPU (tools/emulate_sharded.py): an
     in-process loopback group runs every rank's kernels back to back with direct peer stores
     between the ranks' buffers; group step / P is the compute one rank does in a real 8-GPU
-    step (communication excluded), compared with the single-GPU C4 step / P."""
+    step (communication excluded), compared with the single-GPU C4 step / P.  Self-checking:
+    three i_d planes of every rank's slab after the warm + timed steps are compared with a
+    single-GPU run of the same steps (relative inf-norm)."""
     import inputs
     if not c4_one:
         return None
+    cfg = config_dict("C4")
+    tau = cfg["T"] / cfg["m"]
+    grp, Ug = None, None
     try:
-        cfg = config_dict("C4")
         grp = kx.Group(P, stream=stream)
         for r in range(P):
             pr = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0, slab=(r, P))
-            setup_ctx(kx, pr, cfg["scheme"], cfg["T"] / cfg["m"], stream, ctx=grp.ctx[r])
+            setup_ctx(kx, pr, cfg["scheme"], tau, stream, ctx=grp.ctx[r])
         grp.set_p2p(True)
         Ug = [[torch.from_numpy(u.copy()).cuda() for u in
                inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0, slab=(r, P)).U0]
               for r in range(P)]
-        for _ in range(2):
+        for _ in range(warm):
             grp.step(Ug)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -411,16 +460,50 @@ def emulate_sharded_p8(kx, torch, stream, c4_one, P=8, steps=3):
             e1.record()
         e1.synchronize()
         per_rank = e0.elapsed_time(e1) / steps / P
-        grp.close()
-        del Ug
-        torch.cuda.empty_cache()
-        one = c4_one["ms_per_step"]
-        return {"ranks": P, "per_rank_compute_ms": round(per_rank, 3), "single_gpu_ms": one,
-                "compute_efficiency": round(one / (P * per_rank), 3),
-                "note": "one-GPU emulation (loopback group, direct peer stores): the compute of one "
-                        "rank of an 8-GPU C4 step; communication not included"}
+        n = cfg["n"]
+        plane = n * n
+        loc = n // P                       # i_d planes per rank
+        picks = [0, loc // 2, loc - 1]
+        sample = {(r, c): Ug[r][c].view(loc, plane)[picks].cpu().numpy()
+                  for r in range(P) for c in range(2)}
     except Exception as e:   # the emulation is an extra; it never takes the headline down
         return {"error": str(e)[:200]}
+    finally:
+        if grp is not None:
+            grp.close()
+        del Ug
+        torch.cuda.empty_cache()
+    one = c4_one["ms_per_step"]
+    out = {"ranks": P, "per_rank_compute_ms": round(per_rank, 3), "single_gpu_ms": one,
+           "compute_efficiency": round(one / (P * per_rank), 3),
+           "note": "one-GPU emulation (loopback group, direct peer stores): the compute of one "
+                   "rank of an 8-GPU C4 step; communication not included"}
+    ctx, U = None, None
+    try:   # the same warm + timed steps on one GPU, compared at the sampled planes
+        prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
+        ctx, _ = setup_ctx(kx, prob, cfg["scheme"], tau, stream)
+        U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
+        del prob
+        for _ in range(warm + steps):
+            ctx.step(U)
+        ctx.sync()
+        err, scale = 0.0, 0.0
+        for (r, c), got in sample.items():
+            ref = U[c].view(n, plane)[[r * loc + k for k in picks]].cpu().numpy()
+            err = max(err, float(np.max(np.abs(got - ref))))
+            scale = max(scale, float(np.max(np.abs(ref))))
+        rel = err / scale
+        out["check"] = {"vs": f"single-GPU C4 after the same {warm + steps} steps",
+                        "sampled_points": int(sum(v.size for v in sample.values())),
+                        "rel_inf_err": rel, "tol": 1e-12, "pass": bool(rel <= 1e-12)}
+    except Exception as e:
+        out["check"] = {"error": str(e)[:200]}
+    finally:
+        if ctx is not None:
+            ctx.close()
+        del U
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_kx(args, rank, world, sharded):
@@ -646,6 +729,11 @@ def main():
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
         dist.init_process_group("nccl")
     sharded = args.mode == "sharded" or (world > 1 and args.mode == "auto" and cfg["d"] == 3)
+    if rank == 0:
+        load_peak()   # the roofline denominator, measured on this GPU before the timed region
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
     res, cfg, prob = run_kx(args, rank, world, sharded)
     extra_sharded = None
     if world > 1 and not sharded and not args.no_extras and args.mode == "auto":
@@ -657,7 +745,7 @@ def main():
         return 0
     value = (1 if sharded else world) * 1e3 / res["ms"]
     prof = res["prof"]
-    peak, hbm = load_peak()
+    peak, hbm, peak_src = load_peak()
     achieved = prof["gemm_flops"] / prof["gemm_ms"] / 1e9 if prof["gemm_ms"] > 0 else None
     launches = res["cnt"]["gemm_launches"] + res["cnt"]["other_launches"]
     gemm_launches = prof["gemm_launches"]
@@ -680,9 +768,7 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if (achieved and peak) else None,
                      "traffic": traffic,
-                     "peak_source": "measured fp64 DMMA, 1.5 s sustained on 148 SMs "
-                                    "(tools/peaks.cu -> profiles/peaks_r01.json); MEASURED_PEAKS.json "
-                                    "has no fp64 entry (bf16 sustained x nominal 45/2250 would give 28.0)",
+                     "peak_source": peak_src,
                      "measured_over": "a second pass of the same K steps with a CUDA-event pair "
                                       "around every kernel (event-record nodes in the step graph)",
                      "gemm_share_of_step": prof["gemm_ms"] / (res["prof_ms"] * args.steps),
@@ -699,12 +785,17 @@ def main():
         line["e2e"] = {"value": (1 if sharded else world) * 1e3 / res["e2e_ms"], "unit": "steps/s",
                        "h2d_bytes_per_step": res["e2e_bytes"], "d2h_bytes_per_step": res["e2e_bytes"]}
     if "tucker" in res:
-        line["tucker_tflops"] = res["tucker"]
+        tk = res["tucker"]
+        line["tucker_tflops"] = tk["single"]
+        line["tucker_single_us"] = tk["single_us"]
+        line["tucker_batched_tflops"] = tk["batched"]
+        line["tucker_batch_size"] = tk["batch"]
         line["other_workloads"] = res.get("others")
         if res.get("emulated"):
             line["sharded_c4_emulated"] = res["emulated"]
         if peak:
-            line["tucker_frac_of_dmma"] = {k: round(v / peak, 3) for k, v in res["tucker"].items()}
+            line["tucker_frac_of_dmma"] = {k: round(v / peak, 3) for k, v in tk["single"].items()}
+            line["tucker_batched_frac_of_dmma"] = {k: round(v / peak, 3) for k, v in tk["batched"].items()}
     if not args.no_extras and prob.N <= 64 * 1024 * 1024:
         v, cores, sample = oracle_sample(args.config, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": "steps/s", "cores": cores, "kind": "oracle",

@@ -31,6 +31,9 @@
  *    (KX_ERR_CUDA).  A context is single-stream and not thread-safe; distinct contexts are
  *    independent.
  *  - Aliasing: input tensors must not alias output tensors unless stated.
+ *  - Devices: every call that takes a context runs on that context's device and restores the
+ *    caller's current CUDA device before returning; contexts on different devices in one process
+ *    are independent (per-device kernel attributes and occupancy data are kept per device).
  */
 #ifndef KX_H
 #define KX_H
@@ -113,6 +116,17 @@ kx_status kx_mode_product(kx_ctx *ctx, const double *X, double *Y, int mu, const
  * (reading R2).  X and Y distinct. */
 kx_status kx_tucker(kx_ctx *ctx, const double *X, double *Y, const double *const *L,
                     double alpha, double beta);
+/* Batched Tucker operator: nbatch independent tensors sharing the matrices {L_mu},
+ *   Y_b = alpha * (X_b x_1 L[0] ... x_d L[d-1]) + beta * Y_b,   b = 0 .. nbatch-1,
+ * with X_b = X + b*N and Y_b = Y + b*N (nbatch tensors of N doubles back to back, DEVICE).
+ * One GEMM launch per mode for the whole batch (modes d..1): the tensors' outer slabs are one
+ * strided batch for mu >= 2 and one tall matrix of nbatch*N/n_1 rows for mu = 1, so small
+ * grids (n_mu = 256, 512) fill the GPU that a single Tucker cannot (every mode is a
+ * single GEMM).  Library-owned intermediates of nbatch*N doubles are grown on demand (the first
+ * call with a larger batch synchronises the stream).  nbatch*N must stay below 2^31; X, Y
+ * distinct. */
+kx_status kx_tucker_batched(kx_ctx *ctx, int nbatch, const double *X, double *Y,
+                            const double *const *L, double alpha, double beta);
 /* Kronecker-sum action (eq:kronsumv): Y = K_comp X + beta * Y with the context's
  * direction matrices of component comp.  X and Y distinct. */
 kx_status kx_kronsum(kx_ctx *ctx, int comp, const double *X, double *Y, double beta);
@@ -211,6 +225,19 @@ kx_status kx_get_profile_hbm(kx_ctx *ctx, double *other_bytes);
  * KX_ETD3RKDS_CPLX, `term` indexes real planes: 2i = Re, 2i+1 = Im of term i. */
 kx_status kx_get_phi_matrix(kx_ctx *ctx, int comp, int ell, int stage, int term, int mu,
                             double *out_host);
+
+/* Replace one phi-matrix of the current bank by a caller-supplied HOST matrix (column-major
+ * n_mu x n_mu), the inverse of kx_get_phi_matrix with the same (comp, ell, stage, term, mu)
+ * indexing: P_term{mu} = phi_{l_term}(c tau alpha_{term,mu} A^comp_mu) of eq:split2d /
+ * eq:splitnd3 as listed by Algorithms 1-2's "Needed phi-functions"
+ * (P:2212-2228).  Every scaled block derived from it (the eta- and stage-scaled mu = 1 blocks
+ * of eq:exprk3) is re-formed on the device.  Lets the hot path run on an externally
+ * formed bank — e.g. the CPU oracle's — so that its parity is checked independently of the phi
+ * algorithm (SURVEY §8(c) ledger row 8, "shared bank").  Synchronous; drops the cached step
+ * graph; the next kx_set_tau rebuilds the library's own bank.  KX_ERR_INVALID on a bad index
+ * or non-finite entries (nothing changed). */
+kx_status kx_set_phi_matrix(kx_ctx *ctx, int comp, int ell, int stage, int term, int mu,
+                            const double *in_host);
 
 /* Host-only (no device needed): the split coefficients the library uses.
  * scheme KX_ETD2RKDS -> second-order single term; KX_ETD3RKDS_REAL -> Table 1 (d = 2) or

@@ -90,7 +90,27 @@ def build(verbose: bool = False, force: bool = False) -> str:
         cmd = [nvcc()] + ARCH + ["-shared", "-o", OUT] + objs + ["-cudart", "static", "-ldl"]
         run(cmd)
     build_examples()
+    build_tools()
     return OUT
+
+
+def build_tools() -> None:
+    """Standalone CUDA microbenchmarks (tools/*.cu, e.g. the fp64 DMMA / DFMA / HBM peaks that
+    bench.py measures in the same job) -> build/<name>.  Not part of the product path."""
+    tdir = os.path.join(ROOT, "tools")
+    if not os.path.isdir(tdir):
+        return
+    for f in sorted(os.listdir(tdir)):
+        if not f.endswith(".cu"):
+            continue
+        src = os.path.join(tdir, f)
+        exe = os.path.join(ROOT, "build", f[:-3])
+        if not _newer(exe, [src]):
+            continue
+        cmd = [nvcc()] + ARCH + ["-O3", "-std=c++17", "-lineinfo", "-o", exe, src]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"tool build failed: {' '.join(cmd)}\n{r.stderr}")
 
 
 def build_examples() -> None:

@@ -246,12 +246,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NT, 1)
 size_t fused2d_smem_bytes() { return sizeof(Smem); }
 
 cudaError_t launch_fused2d(const Fused2dArgs& a, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[32] = {};   // per-device function attribute
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) dev = 0;
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(fused2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(Smem));
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev] = true;
   }
   fused2d_kernel<<<CL, NT, sizeof(Smem), stream>>>(a);
   return cudaGetLastError();
@@ -360,11 +362,13 @@ bool tucker2d_small_fits(long long n1, long long n2) {
 cudaError_t launch_tucker2d_small(const double* X, double* Y, const double* L1, const double* L2, int n1,
                                   int n2, double alpha, double beta, cudaStream_t stream) {
   const size_t smem = (size_t)(TS_NMAX + 16) * TS_SS * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[32] = {};   // per-device function attribute
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) dev = 0;
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(tucker2d_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev] = true;
   }
   tucker2d_small_kernel<<<(n2 + 7) / 8, TS_NT, smem, stream>>>(X, Y, L1, L2, n1, n2, alpha, beta);
   return cudaGetLastError();

@@ -652,27 +652,42 @@ struct TileChoice {
 // Resident CTAs per SM (register/smem-limited) and relative per-SM efficiency of each config.
 constexpr TileChoice kTiles[3] = {{128, 128, 32, 1, 1.00}, {128, 64, 16, 2, 0.85}, {64, 64, 16, 3, 0.80}};
 
+// Per-device state: the dynamic-smem opt-in is a per-device function attribute, and occupancy /
+// cluster residency are queried per device (contexts on several devices in one process).
+constexpr int kMaxDev = 32;
+int cur_dev() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) dev = 0;
+  return dev;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 struct Prepared {
-  static inline bool done = false;
-  static inline int occ = 1;   // resident CTAs per SM (occupancy API)
+  static inline bool done[kMaxDev] = {};
+  static inline int occ[kMaxDev] = {};   // resident CTAs per SM (occupancy API)
 };
 
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 cudaError_t prepare_cfg() {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
-  if (!P_::done) {
+  const int dev = cur_dev();
+  if (!P_::done[dev]) {
     auto kern = gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C_::NT, C_::SMEM);
     if (e != cudaSuccess) return e;
-    P_::occ = occ < 1 ? 1 : occ;
-    P_::done = true;
+    P_::occ[dev] = occ < 1 ? 1 : occ;
+    P_::done[dev] = true;
   }
   return cudaSuccess;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
+int occ_of() {
+  return Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>::occ[cur_dev()];
 }
 
 int num_sms();
@@ -684,8 +699,15 @@ constexpr int FN_OF() { return WN / 8; }
 // clusters of S CTAs of this configuration that can be resident at once (GPC packing), cached
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER>
 int max_clusters(int S) {
-  static int cache[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  static int cache_all[kMaxDev][9];
+  static bool init[kMaxDev] = {};
   if (S < 1 || S > 8) return 0;
+  const int dev = cur_dev();
+  int* cache = cache_all[dev];
+  if (!init[dev]) {
+    for (int i = 0; i < 9; ++i) cache[i] = -1;
+    init[dev] = true;
+  }
   if (cache[S] < 0) {
     using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
     cudaLaunchConfig_t cfg = {};
@@ -718,7 +740,6 @@ int max_clusters(int S) {
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER>
 double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
   prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
   sc = Sched{};
   sc.tiles_m = (g.M + BM - 1) / BM;
@@ -727,7 +748,7 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
   sc.ktiles = ((g.kseg + BK - 1) / BK) * g.nseg;
   const int nsm = num_sms();
   const long long T = (long long)sc.tiles_m * sc.tiles_n * nz;
-  const long long Gmax = (long long)nsm * P_::occ;
+  const long long Gmax = (long long)nsm * occ_of<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
   const double kt_us = 4.2 * (BM * BN * BK) / (128.0 * 128 * 32) / eff;
   static const double* fix = [] {   // KX_GEMM_FIX="sk_us,cluster_us": tuning experiments only
     static double f[2] = {6.0, 0.5};   // tuned on the size sweep, the Tucker sweep and C2/C3
@@ -748,7 +769,7 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
   }();
   const int partial = FM_OF<BM, WM>() * FN_OF<BN, WN>() * 2 * C_::NT;   // doubles per partial
   for (int S = 8; cs_env && S >= 2 && T * 2 <= Gmax; S /= 2) {
-    if (T * S <= Gmax && kt >= S && (long long)g.kseg * g.nseg >= 128 && partial * 8 <= C_::SMEM &&
+    if (T * S <= Gmax && kt >= S && (long long)g.kseg * g.nseg >= 128 && partial * 8 <= STAGES * (C_::A_ST + C_::B_ST) * 8 &&
         max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(S) >= T) {
       const double t = per_sm(T * S, (kt + S - 1) / S) * kt_us + fix[1];
       if (t < best) {
@@ -789,13 +810,12 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t stream) {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
-  using P_ = Prepared<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
   cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
   if (e != cudaSuccess) return e;
   Sched sc;
   plan_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(g, nz, eff, sc);
   const long long T = (long long)sc.tiles_m * sc.tiles_n * nz;
-  const long long Gmax = (long long)num_sms() * P_::occ;
+  const long long Gmax = (long long)num_sms() * occ_of<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
   static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only
   if (trace)
     fprintf(stderr, "kx-gemm %s M=%d N=%d K=%dx%d nz=%d cfg=%dx%dx%d tiles=%lld kt=%d G=%d dp=%lld sk_units=%lld G_sk=%d csplit=%d (max clusters of 8/4/2: %d/%d/%d) flops=%.4g\n",
@@ -895,13 +915,14 @@ void prepare_layout() {
 }
 
 int num_sms() {
-  static int nsm = 0;   // defined once; declared above for launch_cfg
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
+  static int nsm_of[kMaxDev] = {};   // per device; declared above for launch_cfg
+  const int dev = cur_dev();
+  if (nsm_of[dev] == 0) {
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
+    nsm_of[dev] = nsm;
   }
-  return nsm;
+  return nsm_of[dev];
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

@@ -34,7 +34,10 @@ kx_status kx_create(kx_ctx** out, int device, void* cuda_stream) {
     g_create_error = "device index out of range";
     return KX_ERR_INVALID;
   }
-  e = cudaSetDevice(device);
+  DevGuard dg_(device);   // the caller's current device is restored on return
+  int now = -1;
+  e = cudaGetDevice(&now);
+  if (e == cudaSuccess && now != device) e = cudaErrorInvalidDevice;
   if (e != cudaSuccess) {
     g_create_error = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
     return KX_ERR_CUDA;
@@ -60,8 +63,8 @@ kx_status kx_create(kx_ctx** out, int device, void* cuda_stream) {
 }
 
 void kx_destroy(kx_ctx* c) {
+  DevGuard dg_(c);
   if (!c) return;
-  cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   drop_bank(c);
   for (auto& v : c->A_dev)
@@ -70,6 +73,8 @@ void kx_destroy(kx_ctx* c) {
     for (double* p : v) cudaFree(p);
   if (c->tmp1) cudaFree(c->tmp1);
   if (c->tmp2) cudaFree(c->tmp2);
+  for (double* p : c->btmp)
+    if (p) cudaFree(p);
   for (int s = 0; s < MAXS; ++s)
     if (c->hostU[s]) cudaFree(c->hostU[s]);
   if (c->flag) cudaFree(c->flag);
@@ -92,6 +97,7 @@ void kx_destroy(kx_ctx* c) {
 const char* kx_last_error(const kx_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   if (d < 1 || d > KX_MAXD) return fail(c, KX_ERR_INVALID, "d must be in 1..6");
   if (ncomp < 1 || ncomp > MAXS) return fail(c, KX_ERR_INVALID, "ncomp must be in 1..4");
@@ -103,7 +109,6 @@ kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
     N *= n[mu];
     if (N > (1LL << 31) - 1) return fail(c, KX_ERR_INVALID, "N = prod n_mu exceeds 2^31-1");
   }
-  cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   drop_bank(c);
   for (auto& v : c->A_dev)
@@ -116,6 +121,11 @@ kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
   if (c->tmp1) cudaFree(c->tmp1);
   if (c->tmp2) cudaFree(c->tmp2);
   c->tmp1 = c->tmp2 = nullptr;
+  for (double*& p : c->btmp) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  c->btmp_cap = 0;
   for (int s = 0; s < MAXS; ++s) {
     if (c->hostU[s]) cudaFree(c->hostU[s]);
     c->hostU[s] = nullptr;
@@ -149,6 +159,7 @@ kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
 }
 
 kx_status kx_set_direction_matrix(kx_ctx* c, int comp, int mu, const double* A_host) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
   if (mu < 1 || mu > c->d) return fail(c, KX_ERR_INVALID, "mu out of range 1..d");
@@ -156,7 +167,6 @@ kx_status kx_set_direction_matrix(kx_ctx* c, int comp, int mu, const double* A_h
   const long long n = c->n[mu - 1];
   for (long long i = 0; i < n * n; ++i)
     if (!std::isfinite(A_host[i])) return fail(c, KX_ERR_INVALID, "A has non-finite entries");
-  cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   drop_bank(c);
   c->A_host[comp][mu - 1].assign(A_host, A_host + n * n);
@@ -192,6 +202,7 @@ kx_status kx_set_direction_matrix(kx_ctx* c, int comp, int mu, const double* A_h
 }
 
 kx_status kx_set_model(kx_ctx* c, kx_model model, const double* params, int nparams) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (model == KX_MODEL_NONE) {
     c->model = 0;
@@ -211,6 +222,7 @@ kx_status kx_set_model(kx_ctx* c, kx_model model, const double* params, int npar
 }
 
 kx_status kx_set_tau(kx_ctx* c, double tau, kx_scheme scheme) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (!(tau > 0.0) || !std::isfinite(tau)) return fail(c, KX_ERR_INVALID, "tau must be > 0");
   if (scheme != KX_ETD2RKDS && scheme != KX_ETD3RKDS_REAL && scheme != KX_ETD3RKDS_CPLX)
@@ -222,7 +234,6 @@ kx_status kx_set_tau(kx_ctx* c, double tau, kx_scheme scheme) {
       if (c->A_host[comp][mu - 1].empty())
         return fail(c, KX_ERR_INVALID, "direction matrix (comp " + std::to_string(comp) +
                                            ", mu " + std::to_string(mu) + ") not set");
-  cudaSetDevice(c->device);
   KX_CUDA(c, cudaStreamSynchronize(c->stream));
   c->cur = c->stream;
   kx_status s = set_tau_impl(c, tau, scheme);
@@ -232,6 +243,7 @@ kx_status kx_set_tau(kx_ctx* c, double tau, kx_scheme scheme) {
 
 kx_status kx_mode_product(kx_ctx* c, const double* X, double* Y, int mu, const double* L,
                           double alpha, double beta) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (mu < 1 || mu > c->d)
@@ -250,6 +262,7 @@ kx_status kx_mode_product(kx_ctx* c, const double* X, double* Y, int mu, const d
 
 kx_status kx_tucker(kx_ctx* c, const double* X, double* Y, const double* const* L, double alpha,
                     double beta) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   KX_TRY(check_ptr(c, X, "X"));
@@ -299,7 +312,83 @@ kx_status kx_tucker(kx_ctx* c, const double* X, double* Y, const double* const* 
   return KX_OK;
 }
 
+kx_status kx_tucker_batched(kx_ctx* c, int nbatch, const double* X, double* Y, const double* const* L,
+                            double alpha, double beta) {
+  DevGuard dg_(c);
+  KX_TRY(need_grid(c));
+  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
+  if (nbatch < 0) return fail(c, KX_ERR_INVALID, "nbatch must be >= 0");
+  if (nbatch == 0) return KX_OK;
+  KX_TRY(check_ptr(c, X, "X"));
+  KX_TRY(check_ptr(c, Y, "Y"));
+  if (!L) return fail(c, KX_ERR_INVALID, "L is NULL");
+  for (int mu = 0; mu < c->d; ++mu) KX_TRY(check_ptr(c, L[mu], "L[mu]"));
+  if (X == Y) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
+  const int d = c->d;
+  const long long N = c->tN;
+  if ((double)nbatch * (double)N > 2147483647.0)
+    return fail(c, KX_ERR_INVALID, "nbatch * N exceeds 2^31-1");
+  c->cur = c->stream;
+  const size_t need = d >= 2 ? (size_t)nbatch * (size_t)N : 0;
+  if (need > c->btmp_cap) {
+    KX_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (double*& p : c->btmp) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    c->btmp_cap = 0;
+    std::vector<double*> keep;
+    KX_TRY(dalloc(c, &c->btmp[0], need, keep));
+    if (d >= 3) KX_TRY(dalloc(c, &c->btmp[1], need, keep));
+    c->btmp_cap = need;
+  }
+  // modes d..2: Y_b = L X_b over every (tensor, outer slab) pair — the tensors are contiguous,
+  // so the batch of nbatch x prod_{nu>mu} n_nu slabs has one stride (n_mu prod_{nu<mu} n_nu)
+  const double* src = X;
+  int w = 0;
+  for (int mu = d; mu >= 2; --mu) {
+    const long long nm = c->tn[mu - 1];
+    const long long R = prod_range(c, 1, mu - 1);
+    const long long Bt = prod_range(c, mu + 1, d);
+    GemmArgs g;
+    g.arow = false;
+    g.M = (int)nm;
+    g.N = (int)R;
+    g.kseg = (int)nm;
+    g.lda = nm;
+    g.ldb = R;
+    g.ldc = R;
+    g.nb = (int)(Bt * nbatch);
+    g.sB_b = g.sC_b = nm * R;
+    g.A[0] = L[mu - 1];
+    g.B[0] = src;
+    g.C[0] = c->btmp[w];
+    KX_TRY(run_gemm(c, g));
+    src = c->btmp[w];
+    w ^= 1;
+  }
+  // mode 1: Y_r = X_r L_1^T over all nbatch * N / n_1 rows
+  const long long n1 = c->tn[0];
+  GemmArgs g;
+  g.arow = true;
+  g.M = (int)((long long)nbatch * N / n1);
+  g.N = (int)n1;
+  g.kseg = (int)n1;
+  g.lda = g.ldb = g.ldc = g.ldd = n1;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.A[0] = src;
+  g.B[0] = L[0];
+  g.C[0] = Y;
+  g.D[0] = beta != 0.0 ? Y : nullptr;
+  KX_TRY(run_gemm(c, g));
+  c->cnt.mode_products += (long long)nbatch * d;
+  c->cnt.tucker_ops += nbatch;
+  return KX_OK;
+}
+
 kx_status kx_kronsum(kx_ctx* c, int comp, const double* X, double* Y, double beta) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
@@ -317,12 +406,14 @@ kx_status kx_kronsum(kx_ctx* c, int comp, const double* X, double* Y, double bet
 }
 
 kx_status kx_set_dist_overlap(kx_ctx* c, int on) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   c->overlap = on != 0;
   return KX_OK;
 }
 
 kx_status kx_set_kronsum_mode(kx_ctx* c, int mode) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   if (mode != 0 && mode != 1) return fail(c, KX_ERR_INVALID, "kronsum mode must be 0 or 1");
   if (c->kronsum_mode != mode) drop_graph(c);
@@ -332,6 +423,7 @@ kx_status kx_set_kronsum_mode(kx_ctx* c, int mode) {
 
 kx_status kx_phi_apply(kx_ctx* c, int comp, int ell, int stage, const double* X, double* Y,
                        double alpha, double beta) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
@@ -379,6 +471,7 @@ kx_status kx_phi_apply(kx_ctx* c, int comp, int ell, int stage, const double* X,
 }
 
 kx_status kx_step(kx_ctx* c, double t, double* const* U) {
+  DevGuard dg_(c);
   (void)t;   // both models are autonomous (reading R7)
   KX_TRY(need_grid(c));
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
@@ -395,6 +488,7 @@ kx_status kx_step(kx_ctx* c, double t, double* const* U) {
 }
 
 kx_status kx_set_fused_small(kx_ctx* c, int on) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   if ((c->fused_small != 0) != (on != 0)) drop_graph(c);
   c->fused_small = on != 0;
@@ -416,6 +510,7 @@ kx_status steps_impl(kx_ctx* c, double* const* U, int nsteps) {
 }  // namespace
 
 kx_status kx_step_n(kx_ctx* c, double t0, int nsteps, double* const* U) {
+  DevGuard dg_(c);
   (void)t0;
   KX_TRY(need_grid(c));
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
@@ -435,6 +530,7 @@ kx_status kx_step_n(kx_ctx* c, double t0, int nsteps, double* const* U) {
 }
 
 kx_status kx_integrate_host(kx_ctx* c, double t0, int nsteps, double* const* U_host) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
@@ -457,18 +553,21 @@ kx_status kx_integrate_host(kx_ctx* c, double t0, int nsteps, double* const* U_h
 }
 
 kx_status kx_get_counters(const kx_ctx* c, kx_counters* out) {
+  DevGuard dg_(c);
   if (!c || !out) return KX_ERR_INVALID;
   *out = c->cnt;
   return KX_OK;
 }
 
 kx_status kx_reset_counters(kx_ctx* c) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   c->cnt = kx_counters{};
   return KX_OK;
 }
 
 kx_status kx_sync(kx_ctx* c) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   KX_CUDA(c, cudaStreamSynchronize(c->stream));
   KX_CUDA(c, cudaGetLastError());
@@ -483,6 +582,7 @@ kx_status kx_sync(kx_ctx* c) {
 }
 
 kx_status kx_set_nan_check(kx_ctx* c, int on) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   if (!c->watch) KX_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&c->watch), 2 * sizeof(int)));
   const int init[2] = {0, -1};
@@ -493,6 +593,7 @@ kx_status kx_set_nan_check(kx_ctx* c, int on) {
 }
 
 kx_status kx_check_finite(kx_ctx* c, const double* X) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   KX_TRY(check_ptr(c, X, "X"));
   int h = 0;
@@ -505,6 +606,7 @@ kx_status kx_check_finite(kx_ctx* c, const double* X) {
 }
 
 kx_status kx_set_profiling(kx_ctx* c, int on) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   KX_TRY(collect_profile(c));
   c->profiling = on != 0;
@@ -517,6 +619,7 @@ kx_status kx_set_profiling(kx_ctx* c, int on) {
 
 kx_status kx_get_profile(kx_ctx* c, double* gemm_ms, double* other_ms, long long* gemm_launches,
                          long long* other_launches, double* gemm_flops) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   KX_TRY(collect_profile(c));
   if (gemm_ms) *gemm_ms = c->prof_ms[0];
@@ -528,6 +631,7 @@ kx_status kx_get_profile(kx_ctx* c, double* gemm_ms, double* other_ms, long long
 }
 
 kx_status kx_get_profile_hbm(kx_ctx* c, double* other_bytes) {
+  DevGuard dg_(c);
   if (!c) return KX_ERR_INVALID;
   KX_TRY(collect_profile(c));
   if (other_bytes) *other_bytes = c->prof_bytes;
@@ -536,6 +640,7 @@ kx_status kx_get_profile_hbm(kx_ctx* c, double* other_bytes) {
 
 kx_status kx_get_phi_matrix(kx_ctx* c, int comp, int ell, int stage, int term, int mu,
                             double* out_host) {
+  DevGuard dg_(c);
   KX_TRY(need_grid(c));
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
   if (comp < 0 || comp >= c->ncomp || mu < 1 || mu > c->d || !out_host)
@@ -557,6 +662,41 @@ kx_status kx_get_phi_matrix(kx_ctx* c, int comp, int ell, int stage, int term, i
     KX_CUDA(c, cudaMemcpy(out_host, G.mid[comp][mu - 1] + t * nm * nm, nm * nm * 8,
                           cudaMemcpyDeviceToHost));
   }
+  return KX_OK;
+}
+
+kx_status kx_set_phi_matrix(kx_ctx* c, int comp, int ell, int stage, int term, int mu,
+                            const double* in_host) {
+  KX_TRY(need_grid(c));
+  DevGuard dg_(c);
+  if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
+  if (comp < 0 || comp >= c->ncomp || mu < 1 || mu > c->d || !in_host)
+    return fail(c, KX_ERR_INVALID, "bad arguments");
+  auto it = c->phi.find({ell, stage});
+  if (it == c->phi.end()) return fail(c, KX_ERR_INVALID, "(ell, stage) not in this bank");
+  const PhiStack& ps = it->second;
+  if (term < 0 || term >= ps.nterms) return fail(c, KX_ERR_INVALID, "term out of range");
+  const long long nm = c->n[mu - 1];
+  for (long long i = 0; i < nm * nm; ++i)
+    if (!std::isfinite(in_host[i])) return fail(c, KX_ERR_INVALID, "phi-matrix has non-finite entries");
+  const Group& G = c->groups[ps.group];
+  const int t = ps.t0 + term;   // plane index inside the group
+  KX_CUDA(c, cudaStreamSynchronize(c->stream));
+  drop_graph(c);
+  c->cur = c->stream;
+  if (mu == 1) {
+    KX_CUDA(c, cudaMemcpy(G.last[comp] + t * nm * nm, in_host, nm * nm * 8, cudaMemcpyHostToDevice));
+    // re-form every scaled block derived from this plane (phi stacks and stage stacks)
+    const int pl = c->cplx ? 2 : 1;
+    for (const BlockRecipe& r : c->recipes)
+      if (r.gi == ps.group && r.comp == comp && r.t == t / pl) KX_TRY(form_block(c, c->groups, r));
+  } else if (mu == c->d) {
+    KX_CUDA(c, cudaMemcpy2D(G.first[comp] + t * nm, (size_t)G.nterms * nm * 8, in_host, nm * 8, nm * 8, nm,
+                            cudaMemcpyHostToDevice));
+  } else {
+    KX_CUDA(c, cudaMemcpy(G.mid[comp][mu - 1] + t * nm * nm, in_host, nm * nm * 8, cudaMemcpyHostToDevice));
+  }
+  KX_CUDA(c, cudaStreamSynchronize(c->stream));
   return KX_OK;
 }
 
@@ -637,6 +777,7 @@ kx_status kx_create_group(kx_ctx** ctxs, int nranks, int device, void* cuda_stre
 }
 
 kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const* U) {
+  DevGuard dg_(ctxs && nranks > 0 ? ctxs[0] : nullptr);
   (void)t;
   if (!ctxs || !U || nranks < 1) return KX_ERR_INVALID;
   for (int r = 0; r < nranks; ++r) {
@@ -685,6 +826,7 @@ kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const
 }
 
 kx_status kx_group_set_p2p(kx_ctx* const* ctxs, int nranks, int on) {
+  DevGuard dg_(ctxs && nranks > 0 ? ctxs[0] : nullptr);
   if (!ctxs || nranks < 1 || nranks > kx::kMaxPeers) return KX_ERR_INVALID;
   for (int r = 0; r < nranks; ++r) {
     kx_ctx* c = ctxs[r];
@@ -722,6 +864,7 @@ static double** ipc_slot(kx_ctx* c, int k, int s) {
 }
 
 kx_status kx_dist_ipc_export(kx_ctx* c, void* blob, size_t cap, size_t* len) {
+  DevGuard dg_(c);
   if (!c || !len) return KX_ERR_INVALID;
   if (c->dist != 1) return fail(c, KX_ERR_INVALID, "not an NCCL-distributed context");
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
@@ -737,6 +880,7 @@ kx_status kx_dist_ipc_export(kx_ctx* c, void* blob, size_t cap, size_t* len) {
 }
 
 kx_status kx_dist_ipc_import(kx_ctx* c, const void* blobs, size_t len_each) {
+  DevGuard dg_(c);
   if (!c || !blobs) return KX_ERR_INVALID;
   if (c->dist != 1) return fail(c, KX_ERR_INVALID, "not an NCCL-distributed context");
   if (c->nranks > kx::kMaxPeers) return fail(c, KX_ERR_UNSUPPORTED, "more ranks than kMaxPeers");

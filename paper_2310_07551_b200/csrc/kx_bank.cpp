@@ -155,6 +155,26 @@ kx_status build_chains(kx_ctx* c, long long n_a, bool emb, std::vector<Chain>& c
   return KX_OK;
 }
 
+// Last-mode blocks: the real part of kappa * eta_t * (W_t x_1 P_t{1}) for a complex term is
+//   W_re x_1 Re(kappa eta P) + W_im x_1 (-Im(kappa eta P)),
+// so a term contributes the blocks [Re(kappa eta P); -Im(kappa eta P)] over its two slots.
+kx_status form_block(kx_ctx* c, const std::vector<Group>& groups, const BlockRecipe& r) {
+  const long long n1 = c->n[0];
+  const long long m2 = n1 * n1;
+  const Group& G = groups[r.gi];
+  double* dst = r.dst;
+  if (!c->cplx) {
+    const double* src = G.last[r.comp] + r.t * m2;
+    const double k = r.kre;
+    return run_other(c, [&] { return kx::launch_scale(dst, src, k, m2, c->cur); });
+  }
+  const double* Pre = G.last[r.comp] + (2 * r.t) * m2;
+  const double* Pim = G.last[r.comp] + (2 * r.t + 1) * m2;
+  const double kre = r.kre, kim = r.kim;
+  KX_TRY(run_other(c, [&] { return kx::launch_axpby(dst, kre, Pre, -kim, Pim, m2, c->cur); }));
+  return run_other(c, [&] { return kx::launch_axpby(dst + m2, -kre, Pim, -kim, Pre, m2, c->cur); });
+}
+
 kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
   const int d = c->d, nc = c->ncomp;
   drop_bank(c);
@@ -305,20 +325,18 @@ kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme) {
       }
     }
   }
-  // Last-mode blocks: the real part of kappa * eta_t * (W_t x_1 P_t{1}) for a complex term is
-  //   W_re x_1 Re(kappa eta P) + W_im x_1 (-Im(kappa eta P)),
-  // so a term contributes the blocks [Re(kappa eta P); -Im(kappa eta P)] over its two slots.
+  // every scaled last-mode block is recorded (kx_set_phi_matrix re-forms it from the bank)
+  c->recipes.clear();
   auto put_blocks = [&](double* dst, int gi, int comp, int t, double kre, double kim) -> kx_status {
-    const long long m2 = n1 * n1;
-    const Group& G = groups[gi];
-    if (!cplx) {
-      const double* src = G.last[comp] + t * m2;
-      return run_other(c, [&] { return kx::launch_scale(dst, src, kre, m2, c->cur); });
-    }
-    const double* Pre = G.last[comp] + (2 * t) * m2;
-    const double* Pim = G.last[comp] + (2 * t + 1) * m2;
-    KX_TRY(run_other(c, [&] { return kx::launch_axpby(dst, kre, Pre, -kim, Pim, m2, c->cur); }));
-    return run_other(c, [&] { return kx::launch_axpby(dst + m2, -kre, Pim, -kim, Pre, m2, c->cur); });
+    BlockRecipe r;
+    r.gi = gi;
+    r.t = t;
+    r.comp = comp;
+    r.kre = kre;
+    r.kim = kim;
+    r.dst = dst;
+    c->recipes.push_back(r);
+    return form_block(c, groups, r);
   };
   // phi stacks for kx_phi_apply: (Re part of) sum_t eta_t T(X, P_t)
   auto make_stack = [&](PhiStack& ps, int gi, int t0, int ell) -> kx_status {

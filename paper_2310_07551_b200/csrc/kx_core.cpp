@@ -83,6 +83,7 @@ void drop_bank(kx_ctx* c) {
   free_list(c->ws_allocs);
   c->groups.clear();
   c->phi.clear();
+  c->recipes.clear();
   for (auto& s : c->stages) s = Stage{};
   c->nstages = 0;
   c->bank_ready = false;

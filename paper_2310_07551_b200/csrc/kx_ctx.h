@@ -57,6 +57,12 @@ struct Stage {               // last-mode concatenated-K stage combination
   double* B[MAXS] = {};
 };
 
+struct BlockRecipe {         // one scaled last-mode block: dst = kappa*eta * P_t{1} (Re/Im pair)
+  int gi = 0, t = 0, comp = 0;
+  double kre = 0.0, kim = 0.0;
+  double* dst = nullptr;
+};
+
 struct Chain {               // one phi-matrix family phi_{0,1,2}(sigma * A^c_mu)
   int c = 0, mu = 0;
   double sigma = 0.0;          // real part of the scale
@@ -66,6 +72,7 @@ struct Chain {               // one phi-matrix family phi_{0,1,2}(sigma * A^c_mu
 
 }  // namespace kx::detail
 
+using kx::detail::BlockRecipe;
 using kx::detail::Chain;
 using kx::detail::Group;
 using kx::detail::KX_MAXD;
@@ -106,12 +113,15 @@ struct kx_ctx {
   std::map<std::pair<int, int>, PhiStack> phi;   // (ell, stage)
   Stage stages[3];
   int nstages = 0;
+  std::vector<BlockRecipe> recipes;   // how every stacked last-mode block was formed
   std::vector<double*> bank_allocs;
   int nslots = 0;
 
   // workspaces
   double* tmp1 = nullptr;
   double* tmp2 = nullptr;
+  double* btmp[2] = {};          // kx_tucker_batched intermediates (grown on demand)
+  size_t btmp_cap = 0;           // doubles per btmp buffer
   double* G[MAXS] = {};
   double* F[MAXS] = {};
   double* D[MAXS] = {};
@@ -192,6 +202,26 @@ inline kx_status fail(kx_ctx* c, kx_status s, const std::string& m) {
   return s;
 }
 
+// Every ABI entry point runs on its context's device and leaves the caller's current device as
+// it found it (distinct contexts on distinct devices in one process stay independent).
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const kx_ctx* c) {
+    int cur = -1;
+    if (c && cudaGetDevice(&cur) == cudaSuccess && cur != c->device && cudaSetDevice(c->device) == cudaSuccess)
+      prev = cur;
+  }
+  explicit DevGuard(int device) {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != device && cudaSetDevice(device) == cudaSuccess) prev = cur;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DevGuard(const DevGuard&) = delete;
+  DevGuard& operator=(const DevGuard&) = delete;
+};
+
 #define KX_CUDA(ctx, expr)                                                                \
   do {                                                                                    \
     cudaError_t e_ = (expr);                                                              \
@@ -257,6 +287,7 @@ kx_status enqueue_fused(kx_ctx* c, double* const* U, int nsteps);
 kx_status step_impl(kx_ctx* c, double* const* U);
 // ---- kx_bank.cpp: phi-bank formation
 kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme);
+kx_status form_block(kx_ctx* c, const std::vector<Group>& groups, const BlockRecipe& r);
 // ---- kx_dist.cpp: slab-sharded steps
 struct NcclApi {
   bool ok = false;

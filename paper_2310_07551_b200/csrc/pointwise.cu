@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) nonlin_scalar_kernel(const PointwiseArgs 
         *peer_redirect(a.peer, c, a.out[c] + oi) = MODE == 1 ? -a.G[c][i] : 0.0;
     }
   }
+  if (a.peer.P) __threadfence_system();   // peer stores performed before the kernel completes
 }
 
 __global__ void scale_kernel(double* __restrict__ y, const double* __restrict__ x, double alpha,
@@ -407,12 +408,13 @@ __global__ void watch_finite_kernel(const double* __restrict__ x, long long n, i
 __global__ void watch_tick_kernel(int* mon) { mon[0] += 1; }
 
 int grid_for(long long work, int block) {
-  static int nsm = 0;
-  if (nsm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) nsm = 148;
-  }
+  static int nsm_of[32] = {};   // per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) dev = 0;
+  if (nsm_of[dev] == 0 && (cudaDeviceGetAttribute(&nsm_of[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+                           nsm_of[dev] <= 0))
+    nsm_of[dev] = 148;
+  const int nsm = nsm_of[dev];
   long long blocks = (work + block - 1) / block;
   const long long cap = (long long)nsm * 16;   // 2 waves of 8 resident 256-thread CTAs per SM
   if (blocks > cap) blocks = cap;

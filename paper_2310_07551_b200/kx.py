@@ -57,6 +57,7 @@ _SIGS = {
     "kx_set_tau": (_i, [_vp, _d, _i]),
     "kx_mode_product": (_i, [_vp, _vp, _vp, _i, _vp, _d, _d]),
     "kx_tucker": (_i, [_vp, _vp, _vp, C.POINTER(_vp), _d, _d]),
+    "kx_tucker_batched": (_i, [_vp, _i, _vp, _vp, C.POINTER(_vp), _d, _d]),
     "kx_kronsum": (_i, [_vp, _i, _vp, _vp, _d]),
     "kx_set_kronsum_mode": (_i, [_vp, _i]),
     "kx_phi_apply": (_i, [_vp, _i, _i, _i, _vp, _vp, _d, _d]),
@@ -81,6 +82,7 @@ _SIGS = {
     "kx_get_profile": (_i, [_vp, _dp, _dp, C.POINTER(_ll), C.POINTER(_ll), _dp]),
     "kx_get_profile_hbm": (_i, [_vp, _dp]),
     "kx_get_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
+    "kx_set_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
     "kx_scheme_coefficients": (_i, [_i, _i, _i, C.POINTER(_i), _dp, C.POINTER(_i), _dp]),
     "kx_scheme_coefficients_cplx": (_i, [_i, _i, C.POINTER(_i), _dp, _dp, C.POINTER(_i), _dp, _dp]),
     "kx_version": (C.c_char_p, []),
@@ -93,8 +95,10 @@ for _name, (_res, _args) in _SIGS.items():
     globals()[_name] = _f
 
 
-def _ptr(t) -> int:
-    """Device pointer of a torch tensor (fp64, CUDA, contiguous) or a raw int."""
+def _ptr(t, numel: int | None = None, device: int | None = None) -> int:
+    """Device pointer of a torch tensor (fp64, CUDA, contiguous) or a raw int.  With `numel`
+    the tensor must hold at least that many doubles, with `device` live on that GPU: the raw
+    ABI cannot check sizes, so this wrapper is the place that stops out-of-bounds kernels."""
     if isinstance(t, int):
         return t
     if t.dtype.__repr__() != "torch.float64":
@@ -103,6 +107,10 @@ def _ptr(t) -> int:
         raise TypeError("tensors must live on the GPU")
     if not t.is_contiguous():
         raise TypeError("tensors must be contiguous")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"tensor holds {t.numel()} doubles, the grid needs {numel}")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"tensor on cuda:{t.device.index}, context on cuda:{device}")
     return t.data_ptr()
 
 
@@ -167,6 +175,8 @@ class Context:
             if st != KX_OK:
                 raise KxError(st, kx_create_error().decode())
         self.h = h
+        self.device = device
+        self.nranks = 1 if dist is None else int(dist[2])
         self.d = 0
         self.n: list[int] = []
         self.ncomp = 0
@@ -210,16 +220,42 @@ class Context:
     def set_tau(self, tau: float, scheme: str):
         self._check(kx_set_tau(self.h, tau, SCHEMES[scheme]))
 
+    @property
+    def local_numel(self) -> int:
+        """Doubles per component tensor this context acts on (its slab on a sharded context)."""
+        return int(np.prod(self.n)) // self.nranks if self.n else 0
+
+    def _state(self, U: list) -> list[int]:
+        if len(U) != self.ncomp:
+            raise ValueError(f"{len(U)} state tensors given, the grid has {self.ncomp} components")
+        return [_ptr(u, self.local_numel, self.device) for u in U]
+
+    def _t(self, X) -> int:
+        return _ptr(X, self.local_numel, self.device)
+
     # --- operators (device tensors)
     def mode_product(self, X, Y, mu: int, L, alpha=1.0, beta=0.0):
-        self._check(kx_mode_product(self.h, _ptr(X), _ptr(Y), mu, _ptr(L), alpha, beta))
+        nm = self.n[mu - 1] if self.n and 1 <= mu <= self.d else None
+        self._check(kx_mode_product(self.h, self._t(X), self._t(Y), mu,
+                                    _ptr(L, nm * nm if nm else None, self.device), alpha, beta))
 
     def tucker(self, X, Y, Ls, alpha=1.0, beta=0.0):
-        arr = (C.c_void_p * len(Ls))(*[_ptr(L) for L in Ls])
-        self._check(kx_tucker(self.h, _ptr(X), _ptr(Y), arr, alpha, beta))
+        if len(Ls) != self.d:
+            raise ValueError(f"{len(Ls)} matrices given, the grid has d = {self.d}")
+        arr = (C.c_void_p * len(Ls))(*[_ptr(L, self.n[m] ** 2, self.device) for m, L in enumerate(Ls)])
+        self._check(kx_tucker(self.h, self._t(X), self._t(Y), arr, alpha, beta))
+
+    def tucker_batched(self, X, Y, Ls, nbatch: int, alpha=1.0, beta=0.0):
+        """nbatch independent Tuckers on X[b*N:(b+1)*N] (one launch per mode)."""
+        if len(Ls) != self.d:
+            raise ValueError(f"{len(Ls)} matrices given, the grid has d = {self.d}")
+        arr = (C.c_void_p * len(Ls))(*[_ptr(L, self.n[m] ** 2, self.device) for m, L in enumerate(Ls)])
+        tot = nbatch * self.local_numel
+        self._check(kx_tucker_batched(self.h, nbatch, _ptr(X, tot, self.device), _ptr(Y, tot, self.device),
+                                      arr, alpha, beta))
 
     def kronsum(self, comp: int, X, Y, beta=0.0):
-        self._check(kx_kronsum(self.h, comp, _ptr(X), _ptr(Y), beta))
+        self._check(kx_kronsum(self.h, comp, self._t(X), self._t(Y), beta))
 
     def set_dist_overlap(self, on: bool):
         self._check(kx_set_dist_overlap(self.h, 1 if on else 0))
@@ -228,14 +264,14 @@ class Context:
         self._check(kx_set_kronsum_mode(self.h, 1 if dense else 0))
 
     def phi_apply(self, comp: int, ell: int, stage: int, X, Y, alpha=1.0, beta=0.0):
-        self._check(kx_phi_apply(self.h, comp, ell, stage, _ptr(X), _ptr(Y), alpha, beta))
+        self._check(kx_phi_apply(self.h, comp, ell, stage, self._t(X), self._t(Y), alpha, beta))
 
     def step(self, U: list, t: float = 0.0):
-        arr = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
+        arr = (C.c_void_p * len(U))(*self._state(U))
         self._check(kx_step(self.h, t, arr))
 
     def step_n(self, U: list, nsteps: int, t0: float = 0.0):
-        arr = (C.c_void_p * len(U))(*[_ptr(u) for u in U])
+        arr = (C.c_void_p * len(U))(*self._state(U))
         self._check(kx_step_n(self.h, t0, nsteps, arr))
 
     def ipc_export(self) -> bytes:
@@ -259,12 +295,19 @@ class Context:
     def integrate_host(self, U_host: list[np.ndarray], nsteps: int, t0: float = 0.0):
         """U_host: C-contiguous float64 host arrays (pinned torch tensors work too: pass
         their .numpy()).  Updated in place."""
+        if len(U_host) != self.ncomp:
+            raise ValueError(f"{len(U_host)} state arrays given, the grid has {self.ncomp} components")
         ptrs = []
         for u in U_host:
             if isinstance(u, np.ndarray):
-                assert u.dtype == np.float64 and u.flags.c_contiguous
+                if u.dtype != np.float64 or not u.flags.c_contiguous:
+                    raise TypeError("host arrays must be C-contiguous float64")
+                if u.size < self.local_numel:
+                    raise ValueError(f"host array holds {u.size} doubles, the grid needs {self.local_numel}")
                 ptrs.append(u.ctypes.data)
             else:
+                if u.numel() < self.local_numel:
+                    raise ValueError(f"host tensor holds {u.numel()} doubles, the grid needs {self.local_numel}")
                 ptrs.append(u.data_ptr())
         arr = (C.c_void_p * len(ptrs))(*ptrs)
         self._check(kx_integrate_host(self.h, t0, nsteps, arr))
@@ -276,7 +319,7 @@ class Context:
         self._check(kx_set_nan_check(self.h, 1 if on else 0))
 
     def check_finite(self, X) -> bool:
-        st = kx_check_finite(self.h, _ptr(X))
+        st = kx_check_finite(self.h, self._t(X))
         if st == KX_ERR_NUMERIC:
             return False
         self._check(st)
@@ -310,6 +353,16 @@ class Context:
                                       out.ctypes.data_as(C.POINTER(C.c_double))))
         return out.reshape(n, n, order="F")
 
+    def set_phi_matrix(self, comp: int, ell: int, stage: int, term: int, mu: int, P: np.ndarray):
+        """Replace one phi-matrix of the bank (inverse of phi_matrix; see kx_set_phi_matrix)."""
+        n = self.n[mu - 1]
+        P = np.asarray(P, dtype=np.float64)
+        if P.shape != (n, n):
+            raise ValueError(f"phi-matrix of mode {mu} must be {n} x {n}, got {P.shape}")
+        buf = np.ascontiguousarray(P.T)   # column-major bytes
+        self._check(kx_set_phi_matrix(self.h, comp, ell, stage, term, mu,
+                                      buf.ctypes.data_as(C.POINTER(C.c_double))))
+
 
 class Group:
     """In-process loopback group of `nranks` contexts on one GPU (kx_create_group): the
@@ -326,10 +379,14 @@ class Group:
         self.nranks = nranks
         self._arr = arr
         self.ctx = [Context(device, stream, handle=C.c_void_p(arr[r])) for r in range(nranks)]
+        for c in self.ctx:
+            c.nranks = nranks
 
     def step(self, U: list[list], t: float = 0.0):
         """U[r][c]: device slab of component c on rank r."""
-        flat = [_ptr(u) for Ur in U for u in Ur]
+        if len(U) != self.nranks:
+            raise ValueError(f"{len(U)} rank states given, the group has {self.nranks} ranks")
+        flat = [p for r, Ur in enumerate(U) for p in self.ctx[r]._state(Ur)]
         arr = (C.c_void_p * len(flat))(*flat)
         st = kx_step_group(self._arr, self.nranks, t, arr)
         if st != KX_OK:

@@ -202,6 +202,81 @@ def test_self_convergence_etd2():
     assert 1.75 <= slope <= 2.25, (slope, errs)
 
 
+def test_self_convergence_cplx():
+    """Algorithm 1 with the complex Table 2, real part kept after each
+    stage combination (reading R19): the scheme must still be third order (Fig. 1's slope-3
+    line for exprk3ds_cplx).  A dropped term, a wrong eta/alpha branch or a truncation in the
+    wrong place breaks the order.  The ladder starts at 400 steps: at 200 the complex split is
+    pre-asymptotic (ratios 6.1, 6.9, 7.5 per halving)."""
+    slope, errs = self_convergence_slope("exprk3ds_cplx", [400, 800, 1600])
+    assert 2.75 <= slope <= 3.25, (slope, errs)
+
+
+def phi_cf_c(ell, z):
+    """Closed-form complex scalar phi_ell, written here independently of oracle.phi."""
+    import cmath
+    if z == 0:
+        return 1.0 / math.factorial(ell)
+    e = cmath.exp(z)
+    return [e, (e - 1) / z, (e - 1 - z) / (z * z)][ell]
+
+
+def scalar_split_c(s, ctau, lams):
+    return sum(eta * np.prod([phi_cf_c(li, ctau * al[mu] * lams[mu]) for mu in range(s.d)])
+               for eta, li, al in zip(s.etas, s.inner, s.alphas))
+
+
+@pytest.mark.parametrize("d,n,delta,tau,ks", [(2, 64, 10.0, 1.0 / 3000, (5, 17)),
+                                              (3, 20, 42.1887, 0.015, (2, 3, 7))])
+def test_linear_step_cosine_closed_form_cplx(d, n, delta, tau, ks):
+    """g = 0, cosine-mode data: one exprk3ds_cplx step of the oracle is the scalar
+    Re(1 + tau lam S_1^tau) with S_1^tau = sum_i eta_i prod_mu phi_{l_i}(tau alpha_{i,mu} lam_mu)
+    from the complex Table 2 — eq:exprk3's last line with D3 = 0,
+    Re taken after the stage combination (R19)."""
+    L = 1.0 if d == 2 else math.pi
+    A1 = inputs.laplacian_neumann(n, L, delta)
+    X = unvec(inputs.kron_vec([inputs.cosine_mode(n, k) for k in ks]), [n] * d)
+    lams = [inputs.cosine_eigenvalue(n, L, delta, k) for k in ks]
+    A = [[A1] * d, [A1] * d]
+    bank = exprk3ds_precompute(A, tau, "cplx")
+    U1 = exprk3ds_step([X, X], 0.0, bank, A, zero_g, {})
+    s1 = coeffs.table2(1, d)
+    expect = np.real(1.0 + tau * sum(lams) * scalar_split_c(s1, tau, lams)) * X
+    assert not np.iscomplexobj(U1[0])
+    assert np.max(np.abs(U1[0] - expect)) <= 1e-12 * np.max(np.abs(X))
+
+
+def test_linear_reaction_cosine_recurrence_cplx():
+    """Linear reaction g(u) = sigma u on cosine-mode data: every stage of Algorithm 1 (complex
+    Table 2) acts on the single mode, so the step is a scalar recurrence in
+    (lam, sigma) built from closed-form complex phi values — it checks that the imaginary part
+    is dropped after EACH stage combination (reading R19), which g = 0 cannot see."""
+    n, delta, tau, sigma, ks = 48, 10.0, 1.0 / 200, -3.0, (3, 11)
+    A1 = inputs.laplacian_neumann(n, 1.0, delta)
+    X = unvec(inputs.kron_vec([inputs.cosine_mode(n, k) for k in ks]), [n, n])
+    lams = [inputs.cosine_eigenvalue(n, 1.0, delta, k) for k in ks]
+    lam = sum(lams)
+    A = [[A1, A1], [A1, A1]]
+
+    def g_lin(t, u, v, p):
+        return sigma * u, sigma * v
+
+    bank = exprk3ds_precompute(A, tau, "cplx")
+    U1 = exprk3ds_step([X, X], 0.0, bank, A, g_lin, {})
+    S = {(ell, c): scalar_split_c(coeffs.table2(ell, 2), c * tau, lams)
+         for ell in (1, 2) for c in (1 / 3, 2 / 3, 1.0)}
+    u0, f = 1.0, (lam + sigma)
+    u2 = np.real(u0 + tau / 3 * S[(1, 1 / 3)] * f)
+    u3 = np.real(u0 + 2 * tau / 3 * S[(1, 2 / 3)] * f + 4 * tau / 3 * S[(2, 2 / 3)] * sigma * (u2 - u0))
+    u1 = np.real(u0 + tau * S[(1, 1.0)] * f + 1.5 * tau * S[(2, 1.0)] * sigma * (u3 - u0))
+    # negative control: keeping the imaginary parts of U2, U3 changes u1 by ~1.5e-6 relative
+    v2 = u0 + tau / 3 * S[(1, 1 / 3)] * f
+    v3 = u0 + 2 * tau / 3 * S[(1, 2 / 3)] * f + 4 * tau / 3 * S[(2, 2 / 3)] * sigma * (v2 - u0)
+    v1 = np.real(u0 + tau * S[(1, 1.0)] * f + 1.5 * tau * S[(2, 1.0)] * sigma * (v3 - u0))
+    assert abs(v1 - u1) > 1e-7 * abs(u1)
+    assert np.max(np.abs(U1[0] - u1 * X)) <= 1e-12 * np.max(np.abs(X))
+
+
 def dominant_modes(U, L, kmax=8):
     """Project U - mean onto cos(k pi x / L) products, k_mu <= kmax (SPEC dominant_modes)."""
     n = U.shape
