@@ -226,12 +226,14 @@ class Context:
         return int(np.prod(self.n)) // self.nranks if self.n else 0
 
     def _state(self, U: list) -> list[int]:
+        if not self.n:   # no grid yet: the C side rejects the call (KX_ERR_INVALID)
+            return [_ptr(u) for u in U]
         if len(U) != self.ncomp:
             raise ValueError(f"{len(U)} state tensors given, the grid has {self.ncomp} components")
         return [_ptr(u, self.local_numel, self.device) for u in U]
 
     def _t(self, X) -> int:
-        return _ptr(X, self.local_numel, self.device)
+        return _ptr(X, self.local_numel if self.n else None, self.device)
 
     # --- operators (device tensors)
     def mode_product(self, X, Y, mu: int, L, alpha=1.0, beta=0.0):
