@@ -49,7 +49,7 @@ def test_sm100a_only(sass):
 
 
 def test_mode_product_gemm_uses_fp64_tensor_cores(sass):
-    gemms = _functions(sass, "gemm_kernel")
+    gemms = _functions(sass, r"11gemm_kernelI")   # the fp64 template (not the tf32 kernel)
     assert len(gemms) >= 12          # 3 tile configs x 2 layouts x 2 vector widths (+ peer stores)
     for f in gemms:
         assert "DMMA.8x8x4" in f      # fp64 tensor-core MMA
@@ -68,8 +68,24 @@ def test_small_grid_kernels_use_clusters_and_dmma(sass):
     assert len(tucker) == 1 and "DMMA.8x8x4" in tucker[0]
 
 
-def test_no_half_precision_mma_anywhere(sass):
-    assert "HMMA" not in sass and not re.search(r"UTC\w*MMA", sass)
+def test_no_half_precision_mma_in_fp64_path(sass):
+    """Only the fp32 variant's kernel (tf32x3_gemm_kernel) may use the tcgen05 tensor cores."""
+    rest = _functions(sass, r"^(?!.*tf32x3_gemm_kernel)")
+    assert rest
+    for f in rest:
+        assert "HMMA" not in f and not re.search(r"UTC\w*MMA", f)
+
+
+def test_fp32_gemm_is_tcgen05_with_tma(sass):
+    """fp32 variant: tcgen05 MMA (UTC*MMA) fed by TMA tensor loads (UTMALDG),
+    accumulators read back from TMEM (LDTM), TMEM allocated/freed by the kernel."""
+    f = _functions(sass, r"tf32x3_gemm_kernel")
+    assert len(f) == 1
+    f = f[0]
+    assert re.search(r"UTC\w*MMA", f)
+    assert "UTMALDG" in f
+    assert "LDTM" in f
+    assert "DMMA" not in f
 
 
 def test_peer_store_gemms_fence_at_system_scope(sass):
