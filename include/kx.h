@@ -239,6 +239,30 @@ kx_status kx_get_phi_matrix(kx_ctx *ctx, int comp, int ell, int stage, int term,
 kx_status kx_set_phi_matrix(kx_ctx *ctx, int comp, int ell, int stage, int term, int mu,
                             const double *in_host);
 
+/* ---------------------------------------------------------------- fp32 variant ----- */
+/* The paper's single-precision runs ("CUDA single" columns of Table 5, and
+ * Table 7; the laptop single-precision timings).
+ * Same operators and step schedule as the fp64 calls, on fp32 DEVICE tensors / matrices (same
+ * vec order and column-major conventions), with every mode product on the tcgen05 tensor cores
+ * (kind::tf32) in a three-pass split x = hi + lo of both operands (hi, lo tf32-valued;
+ * AB ~ A_hi B_hi + A_hi B_lo + A_lo B_hi, fp32 accumulation), which keeps fp32 accuracy.
+ * Requirements: one GPU, every n_mu a multiple of 4, 16-byte aligned buffers; otherwise
+ * KX_ERR_UNSUPPORTED / KX_ERR_INVALID with nothing enqueued.  Library-owned fp32 scratch is
+ * grown on demand (the first larger call synchronises the stream).
+ *
+ * mu-mode product: Y = alpha (X x_mu L) + beta Y; X, Y, L fp32, X and Y distinct. */
+kx_status kx_mode_product_f32(kx_ctx *ctx, const float *X, float *Y, int mu, const float *L,
+                              float alpha, float beta);
+/* Tucker operator: Y = alpha (X x_1 L[0] ... x_d L[d-1]) + beta Y, modes applied
+ * d, ..., 1; L a HOST array of d fp32 DEVICE matrices. */
+kx_status kx_tucker_f32(kx_ctx *ctx, const float *X, float *Y, const float *const *L,
+                        float alpha, float beta);
+/* nsteps (>= 0) steps of the scheme set by kx_set_tau (KX_ETD2RKDS or KX_ETD3RKDS_REAL), in place
+ * on the 2 fp32 DEVICE tensors U[c], d in {2, 3}, tridiagonal A_mu (the stencil Kronecker sum),
+ * a built-in model; the phi-matrices are the fp64 bank of kx_set_tau rounded once.  Replays a
+ * cached CUDA graph per step when the U pointers repeat. */
+kx_status kx_step_f32(kx_ctx *ctx, double t0, int nsteps, float *const *U);
+
 /* Host-only (no device needed): the split coefficients the library uses.
  * scheme KX_ETD2RKDS -> second-order single term; KX_ETD3RKDS_REAL -> Table 1 (d = 2) or
  * Table 3 (d >= 3), "+" branch.  Writes *nterms, eta[i], inner_ell[i] and

@@ -1,13 +1,13 @@
 // fp32 precision variant: the pointwise kernels of the fp32 path.
 //
-// Every fp32 operand of the tcgen05 mode-product GEMM (tf32gemm.cu) is stored as two
-// tf32-valued planes hi = rna_tf32(x), lo = rna_tf32(x - hi).  These kernels produce such planes
-// from fp32 or fp64 data (with an optional transpose for the phi-matrices, which the GEMM reads
-// K-major), and run the fp32 first phase / nonlinearity of a step:
+// The static operand of the tcgen05 mode-product GEMM (tf32gemm.cu: the phi-matrices / L) is
+// stored as two tf32-valued planes hi = rna_tf32(x), lo = rna_tf32(x - hi), K-major.  These
+// kernels produce such planes from fp32 or fp64 data (transposing column-major matrices), and run
+// the fp32 first phase / nonlinearity of a step:
 //   G = g(U), F = K U + G        (tridiagonal A_mu: the (2d+1)-point stencil, eq:kronsumv P:636-640)
 //   D = g(U_s) - G
 // with the Schnakenberg / FitzHugh-Nagumo reaction terms evaluated in
-// fp32.  F and D are written only as (hi, lo) planes: their one consumer is the first mode GEMM.
+// fp32.
 #include "kx_internal.h"
 
 namespace kx {
@@ -39,6 +39,16 @@ __global__ void split_f32_kernel(const float* __restrict__ x, float* __restrict_
                                  long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     split(x[i], h[i], l[i]);
+}
+
+// fp32 -> planes of rows x cols blocks; transpose as split_f64_kernel
+__global__ void split_f32_2d_kernel(const float* __restrict__ x, float* __restrict__ h, float* __restrict__ l,
+                                    long long rows, long long cols, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long nn = rows * cols, b = i / nn, r = (i - b * nn) / cols, c = i - b * nn - r * cols;
+    split(x[b * nn + c * rows + r], h[i], l[i]);
+  }
 }
 
 // fp64 -> (hi, lo) fp32 planes of rows x cols blocks; transpose: out[b][r][c] = x[b][c][r]
@@ -78,7 +88,7 @@ __device__ __forceinline__ void g32(int model, const float* p, float u, float v,
   }
 }
 
-// first phase: G = g(U) (fp32), F = K U + G as (hi, lo) planes, tridiagonal A_mu, 2 species
+// first phase: G = g(U), F = K U + G (fp32), tridiagonal A_mu, 2 species
 template <int D>
 __global__ void __launch_bounds__(256) first_phase_f32_kernel(const F32PhaseArgs a) {
   const long long N = a.N;
@@ -111,26 +121,18 @@ __global__ void __launch_bounds__(256) first_phase_f32_kernel(const F32PhaseArgs
         f += acc;
       }
       a.G[s][i] = g[s];
-      float h, l;
-      split(f, h, l);
-      a.Fh[s][i] = h;
-      a.Fl[s][i] = l;
+      a.F[s][i] = f;
     }
   }
 }
 
-// D = g(U_s) - G as (hi, lo) planes, 2 species
+// D = g(U_s) - G, 2 species
 __global__ void __launch_bounds__(256) nonlin_f32_kernel(const F32PhaseArgs a) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.N; i += (long long)gridDim.x * blockDim.x) {
     float g[2];
     g32(a.model, a.p, a.U[0][i], a.U[1][i], g[0], g[1]);
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      float h, l;
-      split(g[s] - a.G[s][i], h, l);
-      a.Fh[s][i] = h;
-      a.Fl[s][i] = l;
-    }
+    for (int s = 0; s < 2; ++s) a.F[s][i] = g[s] - a.G[s][i];
   }
 }
 
@@ -139,6 +141,15 @@ __global__ void __launch_bounds__(256) nonlin_f32_kernel(const F32PhaseArgs a) {
 cudaError_t launch_split_f32(const float* x, float* hi, float* lo, long long n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   split_f32_kernel<<<grid_of(n), 256, 0, s>>>(x, hi, lo, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_f32_2d(const float* x, float* hi, float* lo, long long rows, long long cols, int nbatch,
+                                bool transpose, cudaStream_t s) {
+  const long long total = rows * cols * nbatch;
+  if (total <= 0) return cudaSuccess;
+  if (!transpose) return launch_split_f32(x, hi, lo, total, s);
+  split_f32_2d_kernel<<<grid_of(total), 256, 0, s>>>(x, hi, lo, rows, cols, total);
   return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ void gemm_prepare_all();
 // ============================================================================ C ABI ======
 extern "C" {
 
-const char* kx_version(void) { return "kx 0.1 (sm_100a, fp64 DMMA mode products)"; }
+const char* kx_version(void) { return "kx 0.2 (sm_100a, fp64 DMMA mode products; fp32 on tcgen05 kind::tf32 x3)"; }
 
 const char* kx_create_error(void) { return g_create_error.c_str(); }
 
@@ -67,6 +67,7 @@ void kx_destroy(kx_ctx* c) {
   if (!c) return;
   cudaStreamSynchronize(c->stream);
   drop_bank(c);
+  f32_free(c);
   for (auto& v : c->A_dev)
     for (double* p : v) cudaFree(p);
   for (auto& v : c->A_tri)
@@ -667,8 +668,8 @@ kx_status kx_get_phi_matrix(kx_ctx* c, int comp, int ell, int stage, int term, i
 
 kx_status kx_set_phi_matrix(kx_ctx* c, int comp, int ell, int stage, int term, int mu,
                             const double* in_host) {
-  KX_TRY(need_grid(c));
   DevGuard dg_(c);
+  KX_TRY(need_grid(c));
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
   if (comp < 0 || comp >= c->ncomp || mu < 1 || mu > c->d || !in_host)
     return fail(c, KX_ERR_INVALID, "bad arguments");
@@ -683,6 +684,7 @@ kx_status kx_set_phi_matrix(kx_ctx* c, int comp, int ell, int stage, int term, i
   const int t = ps.t0 + term;   // plane index inside the group
   KX_CUDA(c, cudaStreamSynchronize(c->stream));
   drop_graph(c);
+  f32_drop(c);   // the fp32 planes are re-derived from the changed bank at the next kx_step_f32
   c->cur = c->stream;
   if (mu == 1) {
     KX_CUDA(c, cudaMemcpy(G.last[comp] + t * nm * nm, in_host, nm * nm * 8, cudaMemcpyHostToDevice));

@@ -67,6 +67,7 @@ void free_list(std::vector<double*>& v) {
 }
 
 void drop_graph(kx_ctx* c) {
+  f32_drop_graph(c);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   c->gexec = nullptr;
@@ -78,6 +79,7 @@ void drop_graph(kx_ctx* c) {
 
 void drop_bank(kx_ctx* c) {
   drop_graph(c);
+  f32_drop(c);
   p2p_close(c);   // the peers' mappings point at buffers about to be reallocated
   free_list(c->bank_allocs);
   free_list(c->ws_allocs);

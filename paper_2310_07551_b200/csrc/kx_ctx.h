@@ -63,6 +63,8 @@ struct BlockRecipe {         // one scaled last-mode block: dst = kappa*eta * P_
   double* dst = nullptr;
 };
 
+struct F32State;             // fp32 variant's bank planes, workspaces and graph (kx_f32.cpp)
+
 struct Chain {               // one phi-matrix family phi_{0,1,2}(sigma * A^c_mu)
   int c = 0, mu = 0;
   double sigma = 0.0;          // real part of the scale
@@ -179,6 +181,8 @@ struct kx_ctx {
   std::vector<void*> ipc_open;   // CUDA IPC mappings of the peers' buffers
   double* bar_buf = nullptr;     // scratch of the NCCL barrier
 
+  kx::detail::F32State* f32 = nullptr;   // fp32 variant (kx_*_f32), created on first use
+
   int nan_check = 0;             // per-step NaN/Inf watchdog inside the step graph
   int* watch = nullptr;          // device {steps completed, first bad step or -1}
 
@@ -288,6 +292,10 @@ kx_status step_impl(kx_ctx* c, double* const* U);
 // ---- kx_bank.cpp: phi-bank formation
 kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme);
 kx_status form_block(kx_ctx* c, const std::vector<Group>& groups, const BlockRecipe& r);
+// ---- kx_f32.cpp: fp32 variant
+void f32_drop_graph(kx_ctx* c);   // the captured fp32 step (model / settings changed)
+void f32_drop(kx_ctx* c);         // + its bank planes and workspaces (bank changed)
+void f32_free(kx_ctx* c);         // everything (context destroyed)
 // ---- kx_dist.cpp: slab-sharded steps
 struct NcclApi {
   bool ok = false;

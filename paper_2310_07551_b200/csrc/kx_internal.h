@@ -73,15 +73,19 @@ cudaError_t launch_gemm(const GemmArgs& g, cudaStream_t stream);
 double gemm_flops(const GemmArgs& g);
 
 // fp32 mode-product GEMM on tcgen05 (kind::tf32, three-pass hi/lo split; tf32gemm.cu).
-// Operands are described by 5-D views (element extents / strides, stride[0] = 1) of two
-// tf32-valued planes hi, lo; the kernel reads them through 128-B-swizzled TMA tensor maps.
-//   TF32_COL (mu >= 2, and the concatenated-M first mode):
-//       A (K-major phi-matrix stack): dims (k, m, t, s, 1);  B (MN-major tensor): (n, k, b, t, s)
-//   TF32_ROW (mu = 1, concatenated K over nseg segments of kseg):
-//       A (K-major tensor rows): dims (k, m, seg, s, 1);    B (MN-major stack): (n, kglob, s, 1, 1)
+// kind::tf32 reads K-major operands only, so the two operands take different routes:
+//   S, the "static" operand (phi-matrix / L): two tf32-valued planes hi, lo, K-major, prepared
+//      by the caller (launch_split_f64 / launch_split_f32_2d with transpose);
+//   T, the "tensor" operand: plain fp32 (T.hi; T.lo unused), split by the kernel's converter
+//      warps (and transposed for TF32_COL).
+// Operands are 5-D views (element extents / strides, stride[0] = 1) read through TMA maps:
+//   TF32_COL (mu >= 2, and the concatenated-M first mode):  C = S T
+//       S (K-major phi-matrix stack): dims (k, m, t, s, 1);   T (MN-major tensor): (n, k, b, t, s)
+//   TF32_ROW (mu = 1, concatenated K over nseg segments of kseg; segment j = (j % slo, j / slo),
+//       so two arithmetic progressions of workspace slots form one concatenated K):  C = T S^T
+//       T (K-major tensor rows): dims (k, m, j % slo, j / slo, s);  S (K-major stack): (k, n, j, s, 1)
 //   z = (s * nt + t) * nb + b;  C_z(m, n) = alpha sum_k A B + beta D_z(m, n), with
-//   C_z = C[s] + t sC_t + b sC_b + m ldc + n (same for D), written as fp32 (C) and/or as the
-//   (hi, lo) planes (Ch, Cl) of the next GEMM's operand.
+//   C_z = C[s] + t sC_t + b sC_b + m ldc + n (same for D), fp32.
 // Requirements: every row stride a multiple of 4 floats, 16-B aligned bases (KX_ERR_UNSUPPORTED
 // otherwise, checked by the caller).
 enum { TF32_COL = 0, TF32_ROW = 1 };
@@ -93,11 +97,9 @@ struct Tf32Dim {
 };
 struct Tf32Gemm {
   int kind = TF32_COL;
-  int M = 0, N = 0, kseg = 0, nseg = 1, ns = 1, nt = 1, nb = 1;
-  Tf32Dim A, B;
+  int M = 0, N = 0, kseg = 0, nseg = 1, slo = 1, ns = 1, nt = 1, nb = 1;
+  Tf32Dim S, T;
   float* C[MAXS] = {};
-  float* Ch[MAXS] = {};
-  float* Cl[MAXS] = {};
   const float* D[MAXS] = {};
   long long ldc = 0, ldd = 0, sC_t = 0, sC_b = 0, sD_t = 0, sD_b = 0;
   float alpha = 1.0f, beta = 0.0f;
@@ -106,7 +108,7 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream);
 double tf32_gemm_flops(const Tf32Gemm& g);
 cudaError_t tf32_prepare();
 
-// fp32 pointwise kernels (f32ops.cu).  Operand planes: hi = rna_tf32(x), lo = rna_tf32(x - hi).
+// fp32 pointwise kernels (f32ops.cu).  Static-operand planes: hi = rna_tf32(x), lo = rna_tf32(x - hi).
 struct F32PhaseArgs {
   int d = 0, model = 0;
   long long n[3] = {1, 1, 1};
@@ -114,11 +116,13 @@ struct F32PhaseArgs {
   float p[8] = {};
   const float* U[2] = {};
   float* G[2] = {};          // first phase: written; nonlinearity: read
-  float* Fh[2] = {};         // first phase: F = K U + G; nonlinearity: D = g(U) - G
-  float* Fl[2] = {};
+  float* F[2] = {};          // first phase: F = K U + G; nonlinearity: D = g(U) - G
   const float* tri[2][3] = {};   // [species][mu-1]: lo | di | up (3 n_mu floats)
 };
 cudaError_t launch_split_f32(const float* x, float* hi, float* lo, long long n, cudaStream_t s);
+// fp32 rows x cols blocks (nbatch, contiguous) -> planes; transpose as launch_split_f64
+cudaError_t launch_split_f32_2d(const float* x, float* hi, float* lo, long long rows, long long cols, int nbatch,
+                                bool transpose, cudaStream_t s);
 // rows x cols blocks (nbatch of them, contiguous): out = planes of scale * x, transposed
 // (out[b][r][c] = x[b][c][r], x column-major rows x cols) when `transpose`
 cudaError_t launch_split_f64(const double* x, float* hi, float* lo, long long rows, long long cols, int nbatch,

@@ -2,23 +2,33 @@
 // three-pass split that recovers fp32 accuracy — the precision variant behind the paper's "CUDA
 // single" columns (Table 5, Table 7).
 //
-// Every fp32 operand x is carried as two tf32-valued planes, hi = rna_tf32(x) and
-// lo = rna_tf32(x - hi) (|x - hi - lo| <= 2^-22 |x|), produced by whoever writes the operand
-// (this kernel's epilogue, the fp32 pointwise kernels, the bank conversion).  A product is then
+// Every fp32 operand x is used as two tf32-valued parts, hi = rna_tf32(x) and
+// lo = rna_tf32(x - hi) (|x - hi - lo| <= 2^-22 |x|).  A product is then
 //     A B ~ A_lo B_hi + A_hi B_lo + A_hi B_hi          (3 tf32 MMAs, fp32 accumulate in TMEM)
-// which drops only the A_lo B_lo term (~2^-22 relative).  The mode products need no permutes
-// (P:219-231): the A operand (the phi-matrix stack for mu >= 2, the tensor rows X_r for mu = 1)
-// is K-major and the B operand (the tensor slab X_b for mu >= 2, L^T for mu = 1) is MN-major;
-// tcgen05 reads both directly from 128-B-swizzled shared memory.
+// which drops only the A_lo B_lo term (~2^-22 relative).
 //
-// Structure (one CTA per SM, persistent over output tiles of 128 x 128):
-//   warp 0      TMA producer: per k-tile, 2 loads of A (hi, lo: 128 rows x 32 k) and 8 of B
-//               (hi, lo: 4 chunks of 32 n x 32 k), completion counted on the stage's mbarrier;
-//   warp 1      MMA issuer (one elected thread): 4 k-steps x 3 MMAs (M=128, N=128, K=8) per
-//               k-tile into a double-buffered TMEM accumulator (2 x 128 columns); tcgen05.commit
-//               frees the smem stage and, after the last k-tile, hands the accumulator over;
-//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns per warp, C = alpha acc + beta D,
-//               stored as fp32 and/or as the (hi, lo) planes the next GEMM reads.
+// kind::tf32 reads both operands K-major only (measured: tools/tcgen05_probe.cu, an MN-major B
+// yields zeros), while the mode products need no permutes: for mu >= 2 the tensor
+// slab X_b is MN-major (n contiguous).  So the two operands take different routes:
+//   * the "static" operand — the phi-matrix / L planes (A for mu >= 2, B = L^T for mu = 1) — is
+//     split and laid out K-major once on the host side of a launch (or once per phi bank) and
+//     TMA-loaded (128-B swizzle) straight into the MMA's shared-memory layout;
+//   * the "tensor" operand is TMA-loaded raw (fp32) and converter warps split it into (hi, lo) in
+//     the K-major 128-B-swizzled layout the MMA reads — transposing it for mu >= 2 on the way —
+//     so tensors stay plain fp32 in HBM (4 B per element read, 4 B written).
+//
+// Structure (one CTA per SM, persistent over output tiles of 128 x 128, 320 threads):
+//   warp 0      TMA producer: per k-tile the static planes (2 x 128 x 32) and the raw tensor tile;
+//   warp 1      MMA issuer (one elected thread): 4 k-steps x 3 MMAs (M = N = 128, K = 8) per
+//               k-tile into a FRESH TMEM accumulator (one of 4 x 128 columns) per k-tile;
+//   warps 2..5  converters: raw tensor tile -> (hi, lo) K-major swizzled (double-buffered);
+//   warps 6..9  accumulators + epilogue: every k-tile's partial is read back (tcgen05.ld, 32
+//               lanes x 128 columns per warp) and added in fp32 round-to-nearest in registers
+//               (one output row per thread); after the tile's last k-tile, C = alpha acc + beta D.
+// The per-k-tile read-back is the accuracy fix measured in profiles/f32_accuracy_r02.json: the
+// tensor core's fp32 accumulation is biased (its error grew linearly with K, 19x numpy's fp32
+// sgemm at K = 1024), so the tensor core only ever sums K = 32 products (x3 passes) and the long
+// sums are rounded to nearest.
 #include "kx_internal.h"
 
 #include <cuda.h>
@@ -30,13 +40,14 @@
 namespace kx {
 namespace {
 
-constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3;
-constexpr int T_A_BYTES = TBM * TBK * 4;          // 16 KB per plane
-constexpr int T_B_BYTES = TBN * TBK * 4;          // 16 KB per plane
-constexpr int T_STAGE_BYTES = 2 * (T_A_BYTES + T_B_BYTES);
-constexpr int T_SMEM = TSTAGES * T_STAGE_BYTES + 1024 /* alignment */ + 256 /* barriers */;
-constexpr int T_THREADS = 192;
-constexpr int T_TMEM_COLS = 256;                  // 2 accumulators of 128 fp32 columns
+constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3, TCONV = 2;
+constexpr int T_PLANE = 128 * TBK * 4;                 // 16 KB: one 128 x 32 fp32 tile
+constexpr int T_STAGE_BYTES = 3 * T_PLANE;             // static hi, static lo, raw tensor
+constexpr int T_CONV_BYTES = 2 * T_PLANE;              // converted tensor hi, lo
+constexpr int T_SMEM = TSTAGES * T_STAGE_BYTES + TCONV * T_CONV_BYTES + 1024 /* alignment */ + 256;
+constexpr int T_THREADS = 320;
+constexpr int T_KBUF = 4;                              // per-k-tile partial accumulators in TMEM
+constexpr int T_TMEM_COLS = T_KBUF * TBN;              // 4 x 128 fp32 columns = all of TMEM
 
 __device__ __forceinline__ unsigned su32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -71,24 +82,22 @@ __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, int
       : "memory");
 }
 
-// shared-memory matrix descriptor (tcgen05): start, leading / stride byte offsets (16-B units),
-// version 1 (sm_100), 128-B swizzle
-__device__ __forceinline__ uint64_t sdesc(unsigned saddr, unsigned lbo, unsigned sbo) {
+// shared-memory matrix descriptor (tcgen05), K-major, 128-B swizzle: start, leading / stride
+// byte offsets (16-B units), version 1 (sm_100), layout SWIZZLE_128B
+__device__ __forceinline__ uint64_t sdesc(unsigned saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;   // version
-  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  d |= (uint64_t)(16 >> 4) << 16;     // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;   // SBO: 8-row groups 1 KB apart
+  d |= (uint64_t)1 << 46;             // version
+  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
   return d;
 }
 
-// instruction descriptor: kind::tf32, fp32 accumulate, A K-major, B MN-major, M = 128, N = 128
+// instruction descriptor: kind::tf32, fp32 accumulate, A and B K-major, M = 128, N = 128
 constexpr uint32_t kIdesc = (1u << 4)           // c_format F32
                             | (2u << 7)         // a_format TF32
                             | (2u << 10)        // b_format TF32
-                            | (0u << 15)        // a_major K
-                            | (1u << 16)        // b_major MN
                             | ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(unsigned tmem_d, uint64_t da, uint64_t db, unsigned accumulate) {
@@ -109,15 +118,17 @@ __device__ __forceinline__ float tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
+__device__ __forceinline__ void split4(const float4 x, float4& h, float4& l) {
+  h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+  l = make_float4(tf32_rna(x.x - h.x), tf32_rna(x.y - h.y), tf32_rna(x.z - h.z), tf32_rna(x.w - h.w));
+}
 
 struct Tf32GemmArgs {
-  CUtensorMap mapA_hi, mapA_lo, mapB_hi, mapB_lo;   // 64-B aligned members first
-  int kind, M, N, kseg, nseg, ns, nt, nb, vec4;
+  CUtensorMap mapS_hi, mapS_lo, mapT;   // 64-B aligned members first
+  int kind, M, N, kseg, nseg, slo, ns, nt, nb, vec4;
   float alpha, beta;
   long long ldc, ldd, sC_t, sC_b, sD_t, sD_b;
   float* C[MAXS];
-  float* Ch[MAXS];
-  float* Cl[MAXS];
   const float* D[MAXS];
 };
 
@@ -129,10 +140,10 @@ __device__ __forceinline__ TileCoord tile_coord(const Tf32GemmArgs& p, int tiles
   const int tmn = tiles_m * tiles_n;
   const int z = tl / tmn, r = tl - z * tmn;
   TileCoord c;
-  if (p.kind == TF32_COL) {   // m fastest: consecutive CTAs share the big B panel
+  if (p.kind == TF32_COL) {   // m fastest: consecutive CTAs share the big tensor panel
     c.m0 = (r % tiles_m) * TBM;
     c.n0 = (r / tiles_m) * TBN;
-  } else {                    // n fastest: consecutive CTAs share the big A panel
+  } else {                    // n fastest: consecutive CTAs share the tensor rows
     c.n0 = (r % tiles_n) * TBN;
     c.m0 = (r / tiles_n) * TBM;
   }
@@ -143,29 +154,42 @@ __device__ __forceinline__ TileCoord tile_coord(const Tf32GemmArgs& p, int tiles
   return c;
 }
 
+// K-major 128-B-swizzled byte offset of element k (< 32) of row r (< 128) of a 128 x 32 tile
+__device__ __forceinline__ unsigned kmajor_off(unsigned r, unsigned kchunk) {
+  return (r >> 3) * 1024 + (r & 7) * 128 + ((kchunk ^ (r & 7)) << 4);
+}
+
 __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_constant__ Tf32GemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + TSTAGES * T_STAGE_BYTES);
+  uint8_t* conv = smem + TSTAGES * T_STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(conv + TCONV * T_CONV_BYTES);
   uint64_t* empty = full + TSTAGES;
-  uint64_t* tfull = empty + TSTAGES;    // accumulator ready (MMA -> epilogue), 2 buffers
-  uint64_t* tempty = tfull + 2;         // accumulator drained (epilogue -> MMA)
-  unsigned* tmem_slot = reinterpret_cast<unsigned*>(tempty + 2);
+  uint64_t* cfull = empty + TSTAGES;    // converted tensor buffer ready (converters -> MMA)
+  uint64_t* cempty = cfull + TCONV;     // converted buffer read by the MMAs (MMA -> converters)
+  uint64_t* kfull = cempty + TCONV;     // k-tile partial ready (MMA -> accumulator warps)
+  uint64_t* kempty = kfull + T_KBUF;    // partial read back (accumulator warps -> MMA)
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(kempty + T_KBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
   const int ntiles = tiles_m * tiles_n * p.ns * p.nt * p.nb;
   const int kps = (p.kseg + TBK - 1) / TBK;
   const int ktiles = kps * p.nseg;
+  const bool col = p.kind == TF32_COL;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < TSTAGES; ++i) {
       mbar_init(full + i, 1);
-      mbar_init(empty + i, 1);
+      mbar_init(empty + i, 1 + 4);   // the MMAs' commit + the 4 converter warps
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(tfull + i, 1);
-      mbar_init(tempty + i, 128);
+    for (int i = 0; i < TCONV; ++i) {
+      mbar_init(cfull + i, 4);
+      mbar_init(cempty + i, 1);
+    }
+    for (int i = 0; i < T_KBUF; ++i) {
+      mbar_init(kfull + i, 1);
+      mbar_init(kempty + i, 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -188,130 +212,158 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
         for (int kt = 0; kt < ktiles; ++kt, ++it) {
           const int st = it % TSTAGES, fill = it / TSTAGES;
           if (fill > 0) mbar_wait(empty + st, (fill - 1) & 1);
-          uint8_t* sA = smem + st * T_STAGE_BYTES;
-          uint8_t* sAl = sA + T_A_BYTES;
-          uint8_t* sB = sAl + T_A_BYTES;
-          uint8_t* sBl = sB + T_B_BYTES;
+          uint8_t* sS = smem + st * T_STAGE_BYTES;
           mbar_expect_tx(full + st, T_STAGE_BYTES);
           const int seg = kt / kps, k0 = (kt - seg * kps) * TBK;
-          int a2, a3, b1, b2, b3, b4;
-          if (p.kind == TF32_COL) {
-            a2 = c.t; a3 = c.s;                 // A: (k, m, t, s)
-            b1 = k0; b2 = c.b; b3 = c.t; b4 = c.s;   // B: (n, k, b, t, s)
+          if (col) {
+            // static A (k, m, t, s); tensor B raw (n, k, b, t, s), one 128 x 32 box
+            tma_load5(sS, &p.mapS_hi, k0, c.m0, c.t, c.s, 0, full + st);
+            tma_load5(sS + T_PLANE, &p.mapS_lo, k0, c.m0, c.t, c.s, 0, full + st);
+            tma_load5(sS + 2 * T_PLANE, &p.mapT, c.n0, k0, c.b, c.t, c.s, full + st);
           } else {
-            a2 = seg; a3 = c.s;                 // A: (k, m, seg, s)
-            b1 = seg * p.kseg + k0; b2 = c.s; b3 = 0; b4 = 0;   // B: (n, kglob, s)
-          }
-          tma_load5(sA, &p.mapA_hi, k0, c.m0, a2, a3, 0, full + st);
-          tma_load5(sAl, &p.mapA_lo, k0, c.m0, a2, a3, 0, full + st);
-#pragma unroll
-          for (int j = 0; j < TBN / 32; ++j) {
-            tma_load5(sB + j * 4096, &p.mapB_hi, c.n0 + 32 * j, b1, b2, b3, b4, full + st);
-            tma_load5(sBl + j * 4096, &p.mapB_lo, c.n0 + 32 * j, b1, b2, b3, b4, full + st);
+            // static B (k, n, seg, s); tensor A raw (k, m, seg % slo, seg / slo, s)
+            const int shi = seg / p.slo;
+            tma_load5(sS, &p.mapS_hi, k0, c.n0, seg, c.s, 0, full + st);
+            tma_load5(sS + T_PLANE, &p.mapS_lo, k0, c.n0, seg, c.s, 0, full + st);
+            tma_load5(sS + 2 * T_PLANE, &p.mapT, k0, c.m0, seg - shi * p.slo, shi, c.s, full + st);
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    int it = 0, tcount = 0;
-    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++tcount) {
-      const int buf = tcount & 1, use = tcount >> 1;
-      if (use > 0) mbar_wait(tempty + buf, (use - 1) & 1);   // epilogue drained this buffer
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const unsigned tmem_d = tmem_base + buf * TBN;
+    int it = 0;
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
       for (int kt = 0; kt < ktiles; ++kt, ++it) {
-        const int st = it % TSTAGES;
+        const int st = it % TSTAGES, cb = it % TCONV, kb = it % T_KBUF;
+        if (it >= T_KBUF) mbar_wait(kempty + kb, ((it / T_KBUF) - 1) & 1);   // partial read back
         mbar_wait(full + st, (it / TSTAGES) & 1);
+        mbar_wait(cfull + cb, (it / TCONV) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         if (lane == 0) {
-          const unsigned a = su32(smem + st * T_STAGE_BYTES);
-          const unsigned al = a + T_A_BYTES, b = al + T_A_BYTES, bl = b + T_B_BYTES;
+          const unsigned tmem_d = tmem_base + kb * TBN;
+          const unsigned s_hi = su32(smem + st * T_STAGE_BYTES), s_lo = s_hi + T_PLANE;
+          const unsigned t_hi = su32(conv + cb * T_CONV_BYTES), t_lo = t_hi + T_PLANE;
+          // COL: A = static, B = converted tensor;  ROW: A = converted tensor, B = static
+          const unsigned a_hi = col ? s_hi : t_hi, a_lo = col ? s_lo : t_lo;
+          const unsigned b_hi = col ? t_hi : s_hi, b_lo = col ? t_lo : s_lo;
 #pragma unroll
-          for (int ks = 0; ks < TBK / 8; ++ks) {
-            // A K-major: k-step = 32 B inside the 128-B swizzled row; 8-row groups 1 KB apart
-            // B MN-major: k-step = one 8-row (1 KB) group; 32-wide n chunks 4 KB apart
-            const uint64_t dA = sdesc(a + ks * 32, 16, 1024), dAl = sdesc(al + ks * 32, 16, 1024);
-            const uint64_t dB = sdesc(b + ks * 1024, 4096, 1024), dBl = sdesc(bl + ks * 1024, 4096, 1024);
-            const unsigned acc0 = (kt > 0 || ks > 0) ? 1u : 0u;
-            mma_tf32(tmem_d, dAl, dB, acc0);
-            mma_tf32(tmem_d, dA, dBl, 1u);
-            mma_tf32(tmem_d, dA, dB, 1u);
+          for (int ks = 0; ks < TBK / 8; ++ks) {   // k-step = 32 B inside the 128-B swizzled rows
+            mma_tf32(tmem_d, sdesc(a_lo + ks * 32), sdesc(b_hi + ks * 32), ks > 0 ? 1u : 0u);
+            mma_tf32(tmem_d, sdesc(a_hi + ks * 32), sdesc(b_lo + ks * 32), 1u);
+            mma_tf32(tmem_d, sdesc(a_hi + ks * 32), sdesc(b_hi + ks * 32), 1u);
           }
-          mma_commit(empty + st);                   // smem stage free once these MMAs finish
-          if (kt == ktiles - 1) mma_commit(tfull + buf);   // accumulator complete
+          mma_commit(empty + st);    // static planes free once these MMAs finish
+          mma_commit(cempty + cb);   // converted buffer free
+          mma_commit(kfull + kb);    // this k-tile's partial complete
         }
         __syncwarp();
       }
     }
-  } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
-    const int q = warp & 3;                 // TMEM lane quarter this warp may access
-    int tcount = 0;
-    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++tcount) {
-      const TileCoord c = tile_coord(p, tiles_m, tiles_n, tl);
-      const int buf = tcount & 1, use = tcount >> 1;
-      mbar_wait(tfull + buf, use & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const int m = c.m0 + q * 32 + lane;
-      const long long zoff_c = c.t * p.sC_t + c.b * p.sC_b;
-      const long long zoff_d = c.t * p.sD_t + c.b * p.sD_b;
-      float* C = p.C[c.s];
-      float* Ch = p.Ch[c.s];
-      float* Cl = p.Cl[c.s];
-      const float* D = p.D[c.s];
-      for (int cb = 0; cb < TBN; cb += 32) {
-        unsigned v[32];
-        const unsigned taddr = tmem_base + ((unsigned)(q * 32) << 16) + buf * TBN + cb;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-              "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-              "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-              "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (cb + 32 >= TBN) {   // whole accumulator read: hand the buffer back to the MMA warp
-          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-          mbar_arrive(tempty + buf);
-        }
-        if (m >= p.M) continue;
-        const int n0 = c.n0 + cb;
-        const long long oc = zoff_c + (long long)m * p.ldc + n0;
-        const long long od = zoff_d + (long long)m * p.ldd + n0;
-        const bool full_row = n0 + 32 <= p.N && p.vec4;
-        if (full_row) {
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ converters (warps 2..5)
+    const int ct = threadIdx.x - 64;   // 0..127
+    int it = 0;
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int st = it % TSTAGES, cb = it % TCONV;
+        mbar_wait(full + st, (it / TSTAGES) & 1);
+        if (it >= TCONV) mbar_wait(cempty + cb, ((it / TCONV) - 1) & 1);
+        const uint8_t* raw = smem + st * T_STAGE_BYTES + 2 * T_PLANE;
+        uint8_t* ohi = conv + cb * T_CONV_BYTES;
+        uint8_t* olo = ohi + T_PLANE;
+        if (col) {
+          // raw MN-major [k][n] (512-B rows, unswizzled) -> K-major row n = ct, 8 chunks of 4 k
+          const float* r = reinterpret_cast<const float*>(raw);
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float4 r = make_float4(p.alpha * __uint_as_float(v[j]), p.alpha * __uint_as_float(v[j + 1]),
-                                   p.alpha * __uint_as_float(v[j + 2]), p.alpha * __uint_as_float(v[j + 3]));
-            if (D) {
-              const float4 dd = *reinterpret_cast<const float4*>(D + od + j);
-              r.x += p.beta * dd.x;
-              r.y += p.beta * dd.y;
-              r.z += p.beta * dd.z;
-              r.w += p.beta * dd.w;
-            }
-            if (C) *reinterpret_cast<float4*>(C + oc + j) = r;
-            if (Ch) {
-              const float4 h = make_float4(tf32_rna(r.x), tf32_rna(r.y), tf32_rna(r.z), tf32_rna(r.w));
-              *reinterpret_cast<float4*>(Ch + oc + j) = h;
-              *reinterpret_cast<float4*>(Cl + oc + j) =
-                  make_float4(tf32_rna(r.x - h.x), tf32_rna(r.y - h.y), tf32_rna(r.z - h.z), tf32_rna(r.w - h.w));
-            }
+          for (int kc = 0; kc < TBK / 4; ++kc) {
+            const float4 x = make_float4(r[(4 * kc + 0) * TBN + ct], r[(4 * kc + 1) * TBN + ct],
+                                         r[(4 * kc + 2) * TBN + ct], r[(4 * kc + 3) * TBN + ct]);
+            float4 h, l;
+            split4(x, h, l);
+            const unsigned o = kmajor_off(ct, kc);
+            *reinterpret_cast<float4*>(ohi + o) = h;
+            *reinterpret_cast<float4*>(olo + o) = l;
           }
         } else {
-          for (int j = 0; j < 32 && n0 + j < p.N; ++j) {
-            float r = p.alpha * __uint_as_float(v[j]);
+          // raw already K-major 128-B swizzled (TMA): elementwise split in place of layout
+#pragma unroll
+          for (int i = 0; i < T_PLANE / 16 / 128; ++i) {
+            const unsigned o = (ct + 128 * i) * 16;
+            float4 h, l;
+            split4(*reinterpret_cast<const float4*>(raw + o), h, l);
+            *reinterpret_cast<float4*>(ohi + o) = h;
+            *reinterpret_cast<float4*>(olo + o) = l;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> MMA reads
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(cfull + cb);
+          mbar_arrive(empty + st);   // raw tile consumed
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ accumulate + epilogue (warps 6..9)
+    const int q = warp & 3;                 // TMEM lane quarter this warp may access
+    int it = 0;
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+      const TileCoord c = tile_coord(p, tiles_m, tiles_n, tl);
+      float acc[TBN];
+#pragma unroll
+      for (int j = 0; j < TBN; ++j) acc[j] = 0.0f;
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int kb = it % T_KBUF;
+        mbar_wait(kfull + kb, (it / T_KBUF) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+        for (int cb = 0; cb < TBN; cb += 32) {
+          unsigned v[32];
+          const unsigned taddr = tmem_base + ((unsigned)(q * 32) << 16) + kb * TBN + cb;
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[cb + j] = __fadd_rn(acc[cb + j], __uint_as_float(v[j]));
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(kempty + kb);   // partial buffer free for the MMAs
+      }
+      const int m = c.m0 + q * 32 + lane;
+      if (m >= p.M) continue;
+      const long long oc = c.t * p.sC_t + c.b * p.sC_b + (long long)m * p.ldc + c.n0;
+      const long long od = c.t * p.sD_t + c.b * p.sD_b + (long long)m * p.ldd + c.n0;
+      float* C = p.C[c.s];
+      const float* D = p.D[c.s];
+      if (c.n0 + TBN <= p.N && p.vec4) {
+#pragma unroll
+        for (int j = 0; j < TBN; j += 4) {
+          float4 r = make_float4(p.alpha * acc[j], p.alpha * acc[j + 1], p.alpha * acc[j + 2], p.alpha * acc[j + 3]);
+          if (D) {
+            const float4 dd = *reinterpret_cast<const float4*>(D + od + j);
+            r.x += p.beta * dd.x;
+            r.y += p.beta * dd.y;
+            r.z += p.beta * dd.z;
+            r.w += p.beta * dd.w;
+          }
+          *reinterpret_cast<float4*>(C + oc + j) = r;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < TBN; ++j) {
+          if (c.n0 + j < p.N) {
+            float r = p.alpha * acc[j];
             if (D) r += p.beta * D[od + j];
-            if (C) C[oc + j] = r;
-            if (Ch) {
-              const float h = tf32_rna(r);
-              Ch[oc + j] = h;
-              Cl[oc + j] = tf32_rna(r - h);
-            }
+            C[oc + j] = r;
           }
         }
       }
@@ -342,22 +394,26 @@ EncodeTiled encoder() {
   return fn;
 }
 
-// 5-D fp32 map with a 128-B swizzle; box = {32, box1, 1, 1, 1}
-cudaError_t make_map(CUtensorMap* map, const float* base, const Tf32Dim& d, int box1) {
+// 5-D fp32 map; box = {box0, box1, 1, 1, 1}; swizzle128: 128-B swizzle (box0 = 32)
+cudaError_t make_map(CUtensorMap* map, const float* base, const Tf32Dim& d, int box0, int box1, bool swizzle128) {
   EncodeTiled enc = encoder();
   if (!enc) return cudaErrorNotSupported;
   cuuint64_t dims[5], strides[4];
-  cuuint32_t box[5] = {32, (cuuint32_t)box1, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+  cuuint32_t box[5] = {(cuuint32_t)box0, (cuuint32_t)box1, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
   for (int i = 0; i < 5; ++i) dims[i] = (cuuint64_t)(d.ext[i] < 1 ? 1 : d.ext[i]);
+  long long prev = 1;   // element stride of dim i-1
   for (int i = 1; i < 5; ++i) {
     long long s = d.stride[i];
-    if (s <= 0) s = d.stride[i - 1] * (long long)dims[i - 1];   // unused extent-1 dims
-    if (s <= 0) s = 1;
+    // extent-1 dims are never stepped: give them the packed stride so every stride is a
+    // multiple of 16 B whatever the caller wrote there
+    if (dims[i] == 1 || s <= 0) s = prev * (long long)dims[i - 1];
     strides[i - 1] = (cuuint64_t)s * 4;
-    if (strides[i - 1] % 16) return cudaErrorInvalidValue;
+    if (strides[i - 1] % 16 || strides[i - 1] >= (1ULL << 40)) return cudaErrorInvalidValue;
+    prev = s;
   }
   const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box,
-                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -390,7 +446,8 @@ double tf32_gemm_flops(const Tf32Gemm& g) {
 
 cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
   if (g.M <= 0 || g.N <= 0 || g.ns * g.nt * g.nb <= 0) return cudaSuccess;
-  if (g.kseg <= 0 || g.nseg <= 0) return cudaErrorInvalidValue;
+  if (g.kseg <= 0 || g.nseg <= 0 || (g.kind == TF32_ROW && g.slo > 0 && g.nseg % g.slo != 0))
+    return cudaErrorInvalidValue;
   cudaError_t e = tf32_prepare();
   if (e != cudaSuccess) return e;
   Tf32GemmArgs p;
@@ -399,6 +456,7 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
   p.N = g.N;
   p.kseg = g.kseg;
   p.nseg = g.nseg;
+  p.slo = g.slo < 1 ? 1 : g.slo;
   p.ns = g.ns;
   p.nt = g.nt;
   p.nb = g.nb;
@@ -414,17 +472,17 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
               g.sD_t % 4 == 0 && g.sD_b % 4 == 0;
   for (int s = 0; s < MAXS; ++s) {
     p.C[s] = g.C[s];
-    p.Ch[s] = g.Ch[s];
-    p.Cl[s] = g.Cl[s];
     p.D[s] = g.beta != 0.0f ? g.D[s] : nullptr;
-    for (const void* q : {(const void*)g.C[s], (const void*)g.Ch[s], (const void*)g.Cl[s], (const void*)p.D[s]})
+    for (const void* q : {(const void*)g.C[s], (const void*)p.D[s]})
       vec4 = vec4 && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
   }
   p.vec4 = vec4;
-  if ((e = make_map(&p.mapA_hi, g.A.hi, g.A, TBM)) != cudaSuccess) return e;
-  if ((e = make_map(&p.mapA_lo, g.A.lo, g.A, TBM)) != cudaSuccess) return e;
-  if ((e = make_map(&p.mapB_hi, g.B.hi, g.B, TBK)) != cudaSuccess) return e;
-  if ((e = make_map(&p.mapB_lo, g.B.lo, g.B, TBK)) != cudaSuccess) return e;
+  const int mS = g.kind == TF32_COL ? TBM : TBN;   // static operand rows per tile
+  if ((e = make_map(&p.mapS_hi, g.S.hi, g.S, TBK, mS, true)) != cudaSuccess) return e;
+  if ((e = make_map(&p.mapS_lo, g.S.lo, g.S, TBK, mS, true)) != cudaSuccess) return e;
+  if (g.kind == TF32_COL) e = make_map(&p.mapT, g.T.hi, g.T, TBN, TBK, false);   // raw [k][n]
+  else e = make_map(&p.mapT, g.T.hi, g.T, TBK, TBM, true);                      // raw K-major
+  if (e != cudaSuccess) return e;
   const long long tiles = (long long)((g.M + TBM - 1) / TBM) * ((g.N + TBN - 1) / TBN) * g.ns * g.nt * g.nb;
   const int grid = (int)std::min<long long>(tiles, num_sms_tf32());
   static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only

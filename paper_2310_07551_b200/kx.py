@@ -83,6 +83,9 @@ _SIGS = {
     "kx_get_profile_hbm": (_i, [_vp, _dp]),
     "kx_get_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
     "kx_set_phi_matrix": (_i, [_vp, _i, _i, _i, _i, _i, _dp]),
+    "kx_mode_product_f32": (_i, [_vp, _vp, _vp, _i, _vp, C.c_float, C.c_float]),
+    "kx_tucker_f32": (_i, [_vp, _vp, _vp, C.POINTER(_vp), C.c_float, C.c_float]),
+    "kx_step_f32": (_i, [_vp, _d, _i, C.POINTER(_vp)]),
     "kx_scheme_coefficients": (_i, [_i, _i, _i, C.POINTER(_i), _dp, C.POINTER(_i), _dp]),
     "kx_scheme_coefficients_cplx": (_i, [_i, _i, C.POINTER(_i), _dp, _dp, C.POINTER(_i), _dp, _dp]),
     "kx_version": (C.c_char_p, []),
@@ -95,14 +98,15 @@ for _name, (_res, _args) in _SIGS.items():
     globals()[_name] = _f
 
 
-def _ptr(t, numel: int | None = None, device: int | None = None) -> int:
-    """Device pointer of a torch tensor (fp64, CUDA, contiguous) or a raw int.  With `numel`
-    the tensor must hold at least that many doubles, with `device` live on that GPU: the raw
-    ABI cannot check sizes, so this wrapper is the place that stops out-of-bounds kernels."""
+def _ptr(t, numel: int | None = None, device: int | None = None, dtype: str = "torch.float64") -> int:
+    """Device pointer of a torch tensor (fp64 — fp32 for the *_f32 calls —, CUDA, contiguous) or
+    a raw int.  With `numel` the tensor must hold at least that many elements, with `device` live
+    on that GPU: the raw ABI cannot check sizes, so this wrapper is the place that stops
+    out-of-bounds kernels."""
     if isinstance(t, int):
         return t
-    if t.dtype.__repr__() != "torch.float64":
-        raise TypeError("tensors must be float64")
+    if t.dtype.__repr__() != dtype:
+        raise TypeError(f"tensors must be {dtype[6:]}")
     if not t.is_cuda:
         raise TypeError("tensors must live on the GPU")
     if not t.is_contiguous():
@@ -275,6 +279,29 @@ class Context:
     def step_n(self, U: list, nsteps: int, t0: float = 0.0):
         arr = (C.c_void_p * len(U))(*self._state(U))
         self._check(kx_step_n(self.h, t0, nsteps, arr))
+
+    # --- fp32 variant (tcgen05 kind::tf32, three-pass split; kx_*_f32)
+    def _t32(self, X) -> int:
+        return _ptr(X, self.local_numel if self.n else None, self.device, "torch.float32")
+
+    def mode_product_f32(self, X, Y, mu: int, L, alpha=1.0, beta=0.0):
+        nm = self.n[mu - 1] if self.n and 1 <= mu <= self.d else None
+        self._check(kx_mode_product_f32(self.h, self._t32(X), self._t32(Y), mu,
+                                        _ptr(L, nm * nm if nm else None, self.device, "torch.float32"),
+                                        alpha, beta))
+
+    def tucker_f32(self, X, Y, Ls, alpha=1.0, beta=0.0):
+        if len(Ls) != self.d:
+            raise ValueError(f"{len(Ls)} matrices given, the grid has d = {self.d}")
+        arr = (C.c_void_p * len(Ls))(*[_ptr(L, self.n[m] ** 2, self.device, "torch.float32")
+                                        for m, L in enumerate(Ls)])
+        self._check(kx_tucker_f32(self.h, self._t32(X), self._t32(Y), arr, alpha, beta))
+
+    def step_f32(self, U: list, nsteps: int = 1, t0: float = 0.0):
+        if self.n and len(U) != self.ncomp:
+            raise ValueError(f"{len(U)} state tensors given, the grid has {self.ncomp} components")
+        arr = (C.c_void_p * len(U))(*[self._t32(u) for u in U])
+        self._check(kx_step_f32(self.h, t0, nsteps, arr))
 
     def ipc_export(self) -> bytes:
         """This NCCL rank's receive buffers as CUDA IPC handles (after set_tau)."""
