@@ -168,8 +168,15 @@ kx_status kx_set_fused_small(kx_ctx *ctx, int on);
  * the same direction matrices, model and tau; its tensors U[c] hold the local slab
  * i_d in [rank n_d/P, (rank+1) n_d/P) in vec order (N/P doubles).  kx_step then performs the
  * sharded step with NCCL all-to-all exchanges (ncclSend/ncclRecv groups, fp64) enqueued on the
- * context stream.  The single-GPU operators (kx_mode_product, kx_tucker, kx_kronsum,
- * kx_phi_apply, kx_integrate_host) return KX_ERR_UNSUPPORTED on distributed contexts. */
+ * context stream.
+ * The operators kx_tucker, kx_mode_product and kx_phi_apply also work on NCCL ranks, on the
+ * rank's layout-A slab X, Y (N/P doubles each; the matrices / bank are global): modes 1..d-1
+ * are local; an operator that contracts mode d runs [A] pack by i_1 block -> all-to-all ->
+ * [B] modes d..2 on full fibres -> all-to-all -> [A] mode 1 as one concatenated-K GEMM over the
+ * source ranks' chunks (alpha, beta in its epilogue), so it matches one GPU up to rounding
+ * (BASELINE.json configs[4] at 2-8 GPUs).  Collective: every rank calls it with the
+ * same arguments apart from X, Y.  kx_tucker_batched, kx_kronsum and kx_integrate_host return
+ * KX_ERR_UNSUPPORTED on distributed contexts. */
 /* 128-byte ncclUniqueId (NCCL from the process, dlopen'ed); create on rank 0, broadcast. */
 kx_status kx_nccl_unique_id(void *out128);
 kx_status kx_create_dist(kx_ctx **ctx, int device, void *cuda_stream, const void *nccl_unique_id,
@@ -184,6 +191,14 @@ kx_status kx_create_group(kx_ctx **ctxs, int nranks, int device, void *cuda_stre
  * (SURVEY §8(f) f2); off = one exchange per phase on the context stream. */
 kx_status kx_set_dist_overlap(kx_ctx *ctx, int on);
 kx_status kx_step_group(kx_ctx *const *ctxs, int nranks, double t, double *const *U);
+/* The distributed operators on a loopback group: X[r], Y[r] are rank r's layout-A slabs
+ * (device, N/P doubles); L / the bank as for the one-context calls. */
+kx_status kx_tucker_group(kx_ctx *const *ctxs, int nranks, const double *const *X, double *const *Y,
+                          const double *const *L, double alpha, double beta);
+kx_status kx_mode_product_group(kx_ctx *const *ctxs, int nranks, const double *const *X,
+                                double *const *Y, int mu, const double *L, double alpha, double beta);
+kx_status kx_phi_apply_group(kx_ctx *const *ctxs, int nranks, int comp, int ell, int stage,
+                             const double *const *X, double *const *Y, double alpha, double beta);
 /* Direct peer stores: the kernel producing each exchanged tensor (stencil F,
  * nonlinearity D, the last mode product of every term group) stores block q of its
  * peer-packed output straight into rank q's receive buffer, so the all-to-all becomes a barrier

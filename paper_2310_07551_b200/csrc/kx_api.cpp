@@ -68,6 +68,7 @@ void kx_destroy(kx_ctx* c) {
   cudaStreamSynchronize(c->stream);
   drop_bank(c);
   f32_free(c);
+  dop_free(c);
   for (auto& v : c->A_dev)
     for (double* p : v) cudaFree(p);
   for (auto& v : c->A_tri)
@@ -112,6 +113,7 @@ kx_status kx_set_grid(kx_ctx* c, int d, const long long* n, int ncomp) {
   }
   cudaStreamSynchronize(c->stream);
   drop_bank(c);
+  dop_free(c);
   for (auto& v : c->A_dev)
     for (double* p : v) cudaFree(p);
   for (auto& v : c->A_tri)
@@ -246,7 +248,7 @@ kx_status kx_mode_product(kx_ctx* c, const double* X, double* Y, int mu, const d
                           double alpha, double beta) {
   DevGuard dg_(c);
   KX_TRY(need_grid(c));
-  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
+  if (c->dist == 2) return fail(c, KX_ERR_INVALID, "loopback group members use kx_mode_product_group");
   if (mu < 1 || mu > c->d)
     return fail(c, KX_ERR_INVALID, "mode " + std::to_string(mu) + " outside 1.." + std::to_string(c->d));
   KX_TRY(check_ptr(c, X, "X"));
@@ -254,6 +256,17 @@ kx_status kx_mode_product(kx_ctx* c, const double* X, double* Y, int mu, const d
   KX_TRY(check_ptr(c, L, "L"));
   if (X == Y) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
   c->cur = c->stream;
+  if (c->dist == 1 && mu == c->d) {   // the sharded direction: two all-to-alls (kx_dist_ops.cpp)
+    DistOp op;
+    op.kind = 2;
+    op.X = X;
+    op.Y = Y;
+    op.L[mu - 1] = L;
+    op.alpha = alpha;
+    op.beta = beta;
+    return dist_op_nccl(c, op);
+  }
+  if (c->dist) set_layout(c, false);   // modes 1..d-1 are local to the slab
   const double* Xs[1] = {X};
   double* Ys[1] = {Y};
   const double* Ls[1] = {L};
@@ -265,7 +278,7 @@ kx_status kx_tucker(kx_ctx* c, const double* X, double* Y, const double* const* 
                     double beta) {
   DevGuard dg_(c);
   KX_TRY(need_grid(c));
-  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
+  if (c->dist == 2) return fail(c, KX_ERR_INVALID, "loopback group members use kx_tucker_group");
   KX_TRY(check_ptr(c, X, "X"));
   KX_TRY(check_ptr(c, Y, "Y"));
   if (!L) return fail(c, KX_ERR_INVALID, "L is NULL");
@@ -273,6 +286,17 @@ kx_status kx_tucker(kx_ctx* c, const double* X, double* Y, const double* const* 
   if (X == Y) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
   c->cur = c->stream;
   const int d = c->d;
+  if (c->dist == 1) {   // slab-sharded: [A] pack -> [B] modes d..2 -> [A] concat-K mode 1
+    DistOp op;
+    op.X = X;
+    op.Y = Y;
+    for (int mu = 0; mu < d; ++mu) op.L[mu] = L[mu];
+    op.alpha = alpha;
+    op.beta = beta;
+    KX_TRY(dist_op_nccl(c, op));
+    c->cnt.tucker_ops += 1;
+    return KX_OK;
+  }
   if (d == 2 && c->fused_small && kx::tucker2d_small_fits(c->tn[0], c->tn[1])) {
     // small 2-D grid: both mode products in one launch, the intermediate in shared memory
     const double fl = 2.0 * (double)c->tN * (double)(c->tn[0] + c->tn[1]);
@@ -426,7 +450,7 @@ kx_status kx_phi_apply(kx_ctx* c, int comp, int ell, int stage, const double* X,
                        double alpha, double beta) {
   DevGuard dg_(c);
   KX_TRY(need_grid(c));
-  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
+  if (c->dist == 2) return fail(c, KX_ERR_INVALID, "loopback group members use kx_phi_apply_group");
   if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
   if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
   auto it = c->phi.find({ell, stage});
@@ -437,6 +461,19 @@ kx_status kx_phi_apply(kx_ctx* c, int comp, int ell, int stage, const double* X,
   if (X == Y) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
   c->cur = c->stream;
   const PhiStack& ps = it->second;
+  if (c->dist == 1) {   // slab-sharded (kx_dist_ops.cpp)
+    DistOp op;
+    op.kind = 1;
+    op.X = X;
+    op.Y = Y;
+    op.alpha = alpha;
+    op.beta = beta;
+    op.comp = comp;
+    op.ps = &ps;
+    KX_TRY(dist_op_nccl(c, op));
+    c->cnt.tucker_ops += ps.nterms;
+    return KX_OK;
+  }
   const Group& G = c->groups[ps.group];
   // run on component `comp` only: temporarily view the context as 1 component
   const int saved_nc = c->ncomp;
@@ -800,30 +837,123 @@ kx_status kx_step_group(kx_ctx* const* ctxs, int nranks, double t, double* const
   for (int ph = 0; ph < dist_phases(ctxs[0]); ++ph) {
     for (int r = 0; r < nranks; ++r) KX_TRY(dist_phase(ctxs[r], U + (size_t)r * nc, ph, xs[r]));
     // loopback exchanges: device copies on the shared stream, after every rank's phase
-    for (int r = 0; r < nranks; ++r) {
-      const Exchange& xr = xs[r];
-      if (xr.kind == 2) continue;   // the producers stored straight into the peers
-      if (xr.kind == 1) {   // halo: first plane -> rank-1's upper halo, last plane -> rank+1's lower
-        for (int k = 0; k + 1 < xr.nbuf; k += 2) {
-          if (r > 0)
-            KX_CUDA(ctxs[r], cudaMemcpyAsync(xs[r - 1].recv[k + 1], xr.send[k], xr.count * 8,
-                                             cudaMemcpyDeviceToDevice, ctxs[r]->stream));
-          if (r + 1 < nranks)
-            KX_CUDA(ctxs[r], cudaMemcpyAsync(xs[r + 1].recv[k], xr.send[k + 1], xr.count * 8,
-                                             cudaMemcpyDeviceToDevice, ctxs[r]->stream));
-        }
-        continue;
-      }
-      for (int k = 0; k < xr.nbuf; ++k)
-        for (int q = 0; q < nranks; ++q)
-          KX_CUDA(ctxs[r], cudaMemcpyAsync(xs[q].recv[k] + (size_t)r * xr.count, xr.send[k] + (size_t)q * xr.count,
-                                           xr.count * 8, cudaMemcpyDeviceToDevice, ctxs[r]->stream));
-    }
+    KX_TRY(loopback_exchange(ctxs, nranks, xs));
   }
   for (int r = 0; r < nranks; ++r) {
     KX_TRY(enqueue_watch(ctxs[r], U + (size_t)r * nc));
     ctxs[r]->cnt.steps += 1;
   }
+  return KX_OK;
+}
+
+namespace {
+// Checks shared by the loopback-group operators; every member must be a group rank in order
+// with the same grid and stream.
+kx_status group_members(kx_ctx* const* ctxs, int nranks) {
+  if (!ctxs || nranks < 1) return KX_ERR_INVALID;
+  for (int r = 0; r < nranks; ++r) {
+    kx_ctx* c = ctxs[r];
+    if (!c || c->dist != 2 || c->rank != r || c->nranks != nranks) return KX_ERR_INVALID;
+    KX_TRY(need_grid(c));
+    if (c->N != ctxs[0]->N || c->d != ctxs[0]->d || c->stream != ctxs[0]->stream)
+      return fail(c, KX_ERR_INVALID, "group members differ in grid or stream");
+    c->cur = c->stream;
+  }
+  return KX_OK;
+}
+
+kx_status group_op(kx_ctx* const* ctxs, int nranks, const std::vector<DistOp>& ops) {
+  std::vector<Exchange> xs(nranks);
+  for (int ph = 0; ph < kDistOpPhases; ++ph) {
+    for (int r = 0; r < nranks; ++r) KX_TRY(dist_op_phase(ctxs[r], ops[r], ph, xs[r]));
+    KX_TRY(loopback_exchange(ctxs, nranks, xs));
+  }
+  return KX_OK;
+}
+}  // namespace
+
+kx_status kx_tucker_group(kx_ctx* const* ctxs, int nranks, const double* const* X, double* const* Y,
+                          const double* const* L, double alpha, double beta) {
+  DevGuard dg_(ctxs && nranks > 0 ? ctxs[0] : nullptr);
+  KX_TRY(group_members(ctxs, nranks));
+  if (!X || !Y || !L) return fail(ctxs[0], KX_ERR_INVALID, "X, Y or L is NULL");
+  std::vector<DistOp> ops(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    KX_TRY(check_ptr(ctxs[r], X[r], "X[r]"));
+    KX_TRY(check_ptr(ctxs[r], Y[r], "Y[r]"));
+    if (X[r] == Y[r]) return fail(ctxs[r], KX_ERR_INVALID, "X and Y must be distinct");
+    for (int mu = 0; mu < ctxs[0]->d; ++mu) {
+      KX_TRY(check_ptr(ctxs[r], L[mu], "L[mu]"));
+      ops[r].L[mu] = L[mu];
+    }
+    ops[r].X = X[r];
+    ops[r].Y = Y[r];
+    ops[r].alpha = alpha;
+    ops[r].beta = beta;
+  }
+  KX_TRY(group_op(ctxs, nranks, ops));
+  for (int r = 0; r < nranks; ++r) ctxs[r]->cnt.tucker_ops += 1;
+  return KX_OK;
+}
+
+kx_status kx_mode_product_group(kx_ctx* const* ctxs, int nranks, const double* const* X, double* const* Y,
+                                int mu, const double* L, double alpha, double beta) {
+  DevGuard dg_(ctxs && nranks > 0 ? ctxs[0] : nullptr);
+  KX_TRY(group_members(ctxs, nranks));
+  if (!X || !Y) return fail(ctxs[0], KX_ERR_INVALID, "X or Y is NULL");
+  if (mu < 1 || mu > ctxs[0]->d) return fail(ctxs[0], KX_ERR_INVALID, "mode out of range");
+  KX_TRY(check_ptr(ctxs[0], L, "L"));
+  std::vector<DistOp> ops(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    KX_TRY(check_ptr(ctxs[r], X[r], "X[r]"));
+    KX_TRY(check_ptr(ctxs[r], Y[r], "Y[r]"));
+    if (X[r] == Y[r]) return fail(ctxs[r], KX_ERR_INVALID, "X and Y must be distinct");
+    if (mu < ctxs[r]->d) {   // local to every slab
+      kx_ctx* c = ctxs[r];
+      set_layout(c, false);
+      const double* Xs[1] = {X[r]};
+      double* Ys[1] = {Y[r]};
+      const double* Ls[1] = {L};
+      const double* Ds[1] = {Y[r]};
+      KX_TRY(mode_product_multi(c, 1, Xs, Ys, mu, Ls, alpha, beta, Ds));
+      continue;
+    }
+    ops[r].kind = 2;
+    ops[r].X = X[r];
+    ops[r].Y = Y[r];
+    ops[r].L[mu - 1] = L;
+    ops[r].alpha = alpha;
+    ops[r].beta = beta;
+  }
+  if (mu < ctxs[0]->d) return KX_OK;
+  return group_op(ctxs, nranks, ops);
+}
+
+kx_status kx_phi_apply_group(kx_ctx* const* ctxs, int nranks, int comp, int ell, int stage,
+                             const double* const* X, double* const* Y, double alpha, double beta) {
+  DevGuard dg_(ctxs && nranks > 0 ? ctxs[0] : nullptr);
+  KX_TRY(group_members(ctxs, nranks));
+  if (!X || !Y) return fail(ctxs[0], KX_ERR_INVALID, "X or Y is NULL");
+  std::vector<DistOp> ops(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    kx_ctx* c = ctxs[r];
+    if (!c->bank_ready) return fail(c, KX_ERR_INVALID, "kx_set_tau has not been called");
+    if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
+    auto it = c->phi.find({ell, stage});
+    if (it == c->phi.end()) return fail(c, KX_ERR_INVALID, "(ell, stage) not in this scheme's bank");
+    KX_TRY(check_ptr(c, X[r], "X[r]"));
+    KX_TRY(check_ptr(c, Y[r], "Y[r]"));
+    if (X[r] == Y[r]) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
+    ops[r].kind = 1;
+    ops[r].X = X[r];
+    ops[r].Y = Y[r];
+    ops[r].alpha = alpha;
+    ops[r].beta = beta;
+    ops[r].comp = comp;
+    ops[r].ps = &it->second;
+  }
+  KX_TRY(group_op(ctxs, nranks, ops));
+  for (int r = 0; r < nranks; ++r) ctxs[r]->cnt.tucker_ops += ops[r].ps->nterms;
   return KX_OK;
 }
 

@@ -180,6 +180,10 @@ struct kx_ctx {
   double* peerHhi[kx::kMaxPeers][MAXS] = {};
   std::vector<void*> ipc_open;   // CUDA IPC mappings of the peers' buffers
   double* bar_buf = nullptr;     // scratch of the NCCL barrier
+  // distributed operators (kx_tucker / kx_mode_product / kx_phi_apply on a sharded context):
+  // pack, layout-B input, two layout-B intermediates, received chunks — Nloc doubles each
+  double* dop[5] = {};
+  std::vector<double*> dop_allocs;
 
   kx::detail::F32State* f32 = nullptr;   // fp32 variant (kx_*_f32), created on first use
 
@@ -344,5 +348,20 @@ int dist_phases(const kx_ctx* c);
 kx_status dist_phase(kx_ctx* c, double* const* U, int ph, Exchange& x);
 kx_status nccl_exchange(kx_ctx* c, const Exchange& x, cudaStream_t st);
 kx_status dist_step_nccl(kx_ctx* c, double* const* U);
+// ---- kx_dist_ops.cpp: distributed operators (Tucker, mode product, split phi-action)
+struct DistOp {
+  int kind = 0;                      // 0 Tucker, 1 split phi-action, 2 mode product along mu = d
+  const double* X = nullptr;         // layout-A slab (Nloc doubles)
+  double* Y = nullptr;
+  const double* L[KX_MAXD] = {};     // Tucker matrices / the mode-d matrix in L[d-1]
+  double alpha = 1.0, beta = 0.0;
+  int comp = 0;
+  const PhiStack* ps = nullptr;
+};
+constexpr int kDistOpPhases = 3;
+kx_status dist_op_phase(kx_ctx* c, const DistOp& op, int ph, Exchange& x);
+kx_status dist_op_nccl(kx_ctx* c, const DistOp& op);
+kx_status loopback_exchange(kx_ctx* const* ctxs, int nranks, const std::vector<Exchange>& xs);
+void dop_free(kx_ctx* c);
 
 }  // namespace kx::detail

@@ -225,6 +225,11 @@ cudaError_t launch_axpby(double* Y, double a, const double* X1, double b, const 
 cudaError_t launch_copy2d(double* Y, long long ldy, long long sy, const double* X, long long ldx,
                           long long sx, long long rows, long long cols, int nbatch, double alpha,
                           cudaStream_t s);
+// Same with Y = alpha X + beta Y (beta != 0 reads Y): the peer-chunk pack / unpack of the
+// distributed operators.
+cudaError_t launch_copy2d_axpby(double* Y, long long ldy, long long sy, const double* X, long long ldx,
+                                long long sx, long long rows, long long cols, int nbatch, double alpha,
+                                double beta, cudaStream_t s);
 // Set n x n identity * v into each of nbatch matrices (stride n*n).
 cudaError_t launch_set_identity(double* Y, long long n, int nbatch, double v, cudaStream_t s);
 // flag[0] |= any(!isfinite(X[0..n)))

@@ -90,13 +90,15 @@ __global__ void axpby_kernel(double* __restrict__ y, double a, const double* __r
 
 __global__ void copy2d_kernel(double* __restrict__ y, long long ldy, long long sy,
                               const double* __restrict__ x, long long ldx, long long sx,
-                              long long rows, long long cols, double alpha) {
+                              long long rows, long long cols, double alpha, double beta) {
   const int bz = blockIdx.y;
   const long long total = rows * cols;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / cols, c = i % cols;
-    y[bz * sy + r * ldy + c] = alpha * x[bz * sx + r * ldx + c];
+    double* yp = y + bz * sy + r * ldy + c;
+    const double v = alpha * x[bz * sx + r * ldx + c];
+    *yp = beta != 0.0 ? v + beta * *yp : v;
   }
 }
 
@@ -497,7 +499,16 @@ cudaError_t launch_copy2d(double* Y, long long ldy, long long sy, const double* 
                           cudaStream_t s) {
   if (rows <= 0 || cols <= 0 || nbatch <= 0) return cudaSuccess;
   dim3 grid(grid_for(rows * cols, 256), nbatch);
-  copy2d_kernel<<<grid, 256, 0, s>>>(Y, ldy, sy, X, ldx, sx, rows, cols, alpha);
+  copy2d_kernel<<<grid, 256, 0, s>>>(Y, ldy, sy, X, ldx, sx, rows, cols, alpha, 0.0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy2d_axpby(double* Y, long long ldy, long long sy, const double* X, long long ldx,
+                                long long sx, long long rows, long long cols, int nbatch, double alpha,
+                                double beta, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0 || nbatch <= 0) return cudaSuccess;
+  dim3 grid(grid_for(rows * cols, 256), nbatch);
+  copy2d_kernel<<<grid, 256, 0, s>>>(Y, ldy, sy, X, ldx, sx, rows, cols, alpha, beta);
   return cudaGetLastError();
 }
 

@@ -69,6 +69,9 @@ _SIGS = {
     "kx_create_dist": (_i, [C.POINTER(_vp), _i, _vp, _vp, _i, _i]),
     "kx_create_group": (_i, [C.POINTER(_vp), _i, _i, _vp]),
     "kx_step_group": (_i, [C.POINTER(_vp), _i, _d, C.POINTER(_vp)]),
+    "kx_tucker_group": (_i, [C.POINTER(_vp), _i, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _d, _d]),
+    "kx_mode_product_group": (_i, [C.POINTER(_vp), _i, C.POINTER(_vp), C.POINTER(_vp), _i, _vp, _d, _d]),
+    "kx_phi_apply_group": (_i, [C.POINTER(_vp), _i, _i, _i, _i, C.POINTER(_vp), C.POINTER(_vp), _d, _d]),
     "kx_group_set_p2p": (_i, [C.POINTER(_vp), _i, _i]),
     "kx_dist_ipc_export": (_i, [_vp, _vp, C.c_size_t, C.POINTER(C.c_size_t)]),
     "kx_dist_ipc_import": (_i, [_vp, _vp, C.c_size_t]),
@@ -420,6 +423,33 @@ class Group:
         st = kx_step_group(self._arr, self.nranks, t, arr)
         if st != KX_OK:
             raise KxError(st, kx_last_error(self.ctx[0].h).decode())
+
+    def _slabs(self, Xs: list) -> "C.Array":
+        if len(Xs) != self.nranks:
+            raise ValueError(f"{len(Xs)} slabs given, the group has {self.nranks} ranks")
+        return (C.c_void_p * self.nranks)(*[self.ctx[r]._t(x) for r, x in enumerate(Xs)])
+
+    def _chk(self, st: int):
+        if st != KX_OK:
+            raise KxError(st, kx_last_error(self.ctx[0].h).decode())
+
+    def tucker(self, Xs: list, Ys: list, Ls: list, alpha=1.0, beta=0.0):
+        """Distributed Tucker operator on the ranks' layout-A slabs (kx_tucker_group)."""
+        c0 = self.ctx[0]
+        if len(Ls) != c0.d:
+            raise ValueError(f"{len(Ls)} matrices given, the grid has d = {c0.d}")
+        L = (C.c_void_p * len(Ls))(*[_ptr(M, c0.n[m] ** 2, c0.device) for m, M in enumerate(Ls)])
+        self._chk(kx_tucker_group(self._arr, self.nranks, self._slabs(Xs), self._slabs(Ys), L, alpha, beta))
+
+    def mode_product(self, Xs: list, Ys: list, mu: int, L, alpha=1.0, beta=0.0):
+        c0 = self.ctx[0]
+        nm = c0.n[mu - 1] if 1 <= mu <= c0.d else None
+        self._chk(kx_mode_product_group(self._arr, self.nranks, self._slabs(Xs), self._slabs(Ys), mu,
+                                        _ptr(L, nm * nm if nm else None, c0.device), alpha, beta))
+
+    def phi_apply(self, comp: int, ell: int, stage: int, Xs: list, Ys: list, alpha=1.0, beta=0.0):
+        self._chk(kx_phi_apply_group(self._arr, self.nranks, comp, ell, stage, self._slabs(Xs),
+                                     self._slabs(Ys), alpha, beta))
 
     def set_p2p(self, on: bool):
         """Direct peer stores instead of exchange copies (after every member's set_tau)."""

@@ -416,8 +416,8 @@ def test_nccl_single_rank_dist_context(kx, overlap, scheme):
     one.sync()
     for s in range(2):
         assert relerr(Ud[s].cpu().numpy(), U1[s].cpu().numpy()) <= 1e-13
-    with pytest.raises(kx.KxError, match="distributed"):
-        dctx.tucker(Ud[0], U1[0], [dmat(np.eye(m)) for m in prob.n])
+    with pytest.raises(kx.KxError, match="distributed"):   # still one-GPU only
+        dctx.tucker_batched(Ud[0], U1[0], [dmat(np.eye(m)) for m in prob.n], 1)
     dctx.close()
     one.close()
 
