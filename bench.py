@@ -266,13 +266,16 @@ def elementwise_roofline(prof):
 
 
 def load_traffic(cfg_name):
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    """DRAM bytes (read + write) of ALL mode-product GEMM launches of one step of this config,
+    from one `ncu --set full` capture (profiles/ncu_gemm_r02.json, tools/ncu_gemm_summary.py),
+    with the algorithmic operand bytes of the same launches: (traffic, alg_bytes) or (None, None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_gemm_r02.json")
     try:
         with open(p) as f:
-            j = json.load(f)
-        return j.get(cfg_name, {}).get("gemm_dram_bytes_per_launch")
+            st = json.load(f)[cfg_name]["step"]
+        return st["dram_bytes"], st.get("alg_bytes")
     except Exception:
-        return None
+        return None, None
 
 
 def setup_ctx(kx, prob, scheme, tau, stream, ctx=None):
@@ -353,6 +356,76 @@ def other_configs(kx, torch, stream, steps=10):
                                                    "us_per_step": round(ms * 1e3, 2),
                                                    "launches": 1, "steps_per_launch": nsteps}
     ctx.close()
+    return out
+
+
+def tf32_peak():
+    """Dense tf32 tensor peak of this pool: MEASURED_PEAKS.json bf16 sustained x the guide's nominal
+    ratio tf32 / bf16 = 1.1 / 2.25 PFLOP/s (B200_PROFILING.md), with the source."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return (float(j["bf16_tflops_sustained"]) * 1.1 / 2.25,
+                "MEASURED_PEAKS.json bf16_tflops_sustained x 1.1/2.25 (nominal tf32/bf16 dense)")
+    except Exception:
+        return 1100.0, "B200_PROFILING.md nominal tf32 dense 1.1 PFLOP/s (MEASURED_PEAKS.json absent)"
+
+
+def f32_workloads(kx, torch, stream, steps=10):
+    """The fp32 variant (the paper's "CUDA single" columns): kx_step_f32 at C2 and
+    C3 (same timing protocol: L2 flushed between steps, CUDA events on the library stream) and its
+    mode-product GEMM (tcgen05 kind::tf32, three passes) against the tf32 tensor peak."""
+    import inputs
+    out = {}
+    peak, src = tf32_peak()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    for cfg_name in ("C2", "C3"):
+        cfg = config_dict(cfg_name)
+        prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=0)
+        ctx, _ = setup_ctx(kx, prob, cfg["scheme"], cfg["T"] / cfg["m"], stream)
+        U = [torch.from_numpy(u.astype("float32")).cuda() for u in prob.U0]
+        ctx.step_f32(U, 3)
+        ctx.sync()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        with torch.cuda.stream(stream):
+            for k in range(steps):
+                flush.fill_(float(k))
+                ev[k][0].record()
+                ctx.step_f32(U, 1)
+                ev[k][1].record()
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+        ctx.set_profiling(True)
+        ctx.step_f32(U, 5)
+        ctx.sync()
+        prof = ctx.profile()
+        ctx.set_profiling(False)
+        alg = prof["gemm_flops"] / prof["gemm_ms"] / 1e9
+        out[cfg_name] = {"workload": cfg["desc"] + " (fp32)", "steps_per_s": round(1e3 / ms, 1),
+                         "ms_per_step": round(ms, 4), "gemm_share": round(prof["gemm_ms"] / (prof["gemm_ms"] + prof["other_ms"]), 3),
+                         "gemm_tflops_fp32_equiv": round(alg, 1),
+                         "gemm_tflops_tensor": round(3 * alg, 1),
+                         "gemm_frac_of_tf32_peak": round(3 * alg / peak, 3),
+                         "finite": all(bool(torch.isfinite(u).all()) for u in U)}
+        ctx.close()
+        del U
+        torch.cuda.empty_cache()
+    # one large Tucker (the GEMM at its best shape)
+    n = 4096
+    ctx = kx.Context(stream.device.index, stream)
+    ctx.set_grid([n, n], 1)
+    X = torch.rand(n * n, device="cuda")
+    Y = torch.empty_like(X)
+    Ls = [torch.rand(n * n, device="cuda") / n] * 2
+    ms = _graph_time(torch, stream, lambda: ctx.tucker_f32(X, Y, Ls), 10)
+    fl = 2.0 * n * n * 2 * n
+    out["tucker_d2_n4096"] = {"ms": round(ms, 4), "tflops_fp32_equiv": round(fl / ms / 1e9, 1),
+                              "frac_of_tf32_peak": round(3 * fl / ms / 1e9 / peak, 3)}
+    ctx.close()
+    out["peak_tf32_tflops"] = round(peak, 1)
+    out["peak_source"] = src
+    out["method"] = ("tcgen05.mma kind::tf32, A B ~ A_lo B_hi + A_hi B_lo + A_hi B_hi (x = hi + lo, tf32 "
+                     "parts), TMA loads, per-k-tile TMEM partials summed round-to-nearest in registers")
     return out
 
 
@@ -506,6 +579,61 @@ def emulate_sharded_p8(kx, torch, stream, c4_one, P=8, steps=3, warm=2):
     return out
 
 
+def sharded_closed_form_check(kx, torch, stream, cfg, n, rank, world, uid, p2p, dist):
+    """Correctness of the sharded step at full size, without an oracle run: g = 0 and cosine-mode
+    data (an eigenvector of every Neumann Laplacian A_mu, inputs.cosine_mode) make one exprk3ds
+    step the scalar recurrence U+ = Re(1 + tau sum_mu lam_mu sum_i eta_i prod_mu
+    phi_{l_i}(tau alpha_{i,mu} lam_mu)) U (eq:exprk3 P:586-594 with F = K U, split eq:splitnd3),
+    evaluated from the library's own Table 3 coefficients (kx_scheme_coefficients); every
+    rank compares its slab, max over ranks."""
+    import cmath
+    import math
+    import inputs
+    tau = cfg["T"] / cfg["m"]
+    d = cfg["d"]
+    ks = (2, 37, 130)[:d]
+    delta = 42.1887 if cfg["model"] == "fhn" else 1.0
+    length = math.pi if cfg["model"] == "fhn" else 1.0
+    A = inputs.laplacian_neumann(n[0], length, delta)
+    lams = [inputs.cosine_eigenvalue(n[mu], length, delta, ks[mu]) for mu in range(d)]
+    modes = [inputs.cosine_mode(n[mu], ks[mu]) for mu in range(d)]
+    ndl = n[-1] // world
+    modes[-1] = modes[-1][rank * ndl:(rank + 1) * ndl]          # this rank's i_d block
+    x = inputs.kron_vec(modes)
+    ctx = kx.Context(torch.cuda.current_device(), stream, dist=(uid, rank, world))
+    try:
+        ctx.set_grid(n, 2)
+        for c in range(2):
+            for mu in range(d):
+                ctx.set_direction_matrix(c, mu + 1, A)
+        ctx.set_model("none")
+        ctx.set_tau(tau, "etd3rkds")
+        etas, inner, alphas = kx.scheme_coefficients("etd3rkds", 1, d)
+
+        def phis(ell, z):
+            e = cmath.exp(z)
+            return [e, (e - 1) / z, (e - 1 - z) / (z * z)][ell]
+
+        split = sum(eta * math.prod(phis(li, tau * al[m] * lams[m]) for m in range(d))
+                    for eta, li, al in zip(etas, inner, alphas))
+        factor = (1.0 + tau * sum(lams) * split).real
+        U = [torch.from_numpy(x.copy()).cuda(), torch.from_numpy(x.copy()).cuda()]
+        ctx.step(U)
+        ctx.sync()
+        got = U[0].cpu().numpy()
+        err = float(abs(got - factor * x).max() / abs(factor * x).max())
+        if dist is not None:
+            t = torch.tensor([err], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            err = float(t.item())
+        return {"what": "one sharded step, g = 0, cosine mode (k = %s), scalar recurrence from Table 3" % (ks,),
+                "rel_inf_err": err, "tol": 1e-11, "pass": err <= 1e-11}
+    except Exception as e:
+        return {"error": str(e)[:300]}
+    finally:
+        ctx.close()
+
+
 def run_kx(args, rank, world, sharded):
     import torch
     import inputs
@@ -534,14 +662,32 @@ def run_kx(args, rank, world, sharded):
         t0 = time.perf_counter()
         ctx.set_tau(tau, cfg["scheme"])
         phi_s = time.perf_counter() - t0
+        exchange = args.exchange
         if args.exchange == "p2p":
-            # direct peer stores: every rank maps the others' receive buffers (CUDA IPC)
-            blobs = [ctx.ipc_export()]
+            # direct peer stores: every rank maps the others' receive buffers (CUDA IPC); if any
+            # rank cannot export or import, every rank falls back to NCCL all-to-alls
+            why = ""
+            try:
+                blob = ctx.ipc_export()
+            except Exception as e:
+                blob, why = None, f"export: {e}"[:200]
+            blobs = [blob]
             if world > 1:
-                allb = [None] * world
-                dist.all_gather_object(allb, blobs[0])
-                blobs = allb
-            ctx.ipc_import(blobs)
+                blobs = [None] * world
+                dist.all_gather_object(blobs, blob)
+            ok = all(b is not None for b in blobs)
+            if ok:
+                try:
+                    ctx.ipc_import(blobs)
+                except Exception as e:
+                    ok, why = False, f"import: {e}"[:200]
+            if world > 1:
+                t = torch.tensor([1 if ok else 0], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MIN)
+                ok = bool(t.item())
+            if not ok:
+                ctx.set_tau(tau, cfg["scheme"])   # drops any partial peer mapping
+                exchange = "nccl (CUDA IPC peer mapping failed" + (f": {why}" if why else " on another rank") + ")"
     else:
         prob = inputs.make_problem(cfg["model"], cfg["d"], cfg["n"], seed=rank)
         ctx, phi_s = setup_ctx(kx, prob, cfg["scheme"], tau, stream)
@@ -603,6 +749,8 @@ def run_kx(args, rank, world, sharded):
     ok = all(ctx.check_finite(u) for u in U)
     res = dict(ms=ms, step_ms=step_ms, prof=prof, prof_ms=prof_ms, cnt=cnt, clocks=clk, phi_s=phi_s,
                finite=ok)
+    if sharded:
+        res["exchange"] = exchange
     # ---- e2e: pinned host state -> device, one step through the public API, device -> host
     if not args.no_extras:
         Uh = [torch.from_numpy(u.copy()).pin_memory() for u in prob.U0]
@@ -633,18 +781,27 @@ def run_kx(args, rank, world, sharded):
         res["e2e_ms"] = e
         res["e2e_bytes"] = 2 * (prob.N // (world if sharded else 1)) * 8
     ctx.close()
+    if sharded and cfg["d"] == 3:   # after the timed context is gone (memory)
+        del U
+        torch.cuda.empty_cache()
+        res["check"] = sharded_closed_form_check(kx, torch, stream, cfg, prob.n, rank, world, uid[0],
+                                                 exchange == "p2p", dist if world > 1 else None)
     if not args.no_extras and rank == 0 and not sharded:
         del U, flush
         torch.cuda.empty_cache()
         res["tucker"] = tucker_sweep(kx, torch, stream)
         res["others"] = other_configs(kx, torch, stream)
+        try:
+            res["f32"] = f32_workloads(kx, torch, stream)
+        except Exception as e:   # the fp64 headline must not depend on the fp32 variant
+            res["f32"] = {"error": str(e)[:300]}
         if world == 1:
             res["emulated"] = emulate_sharded_p8(kx, torch, stream,
                                                  res["others"].get("C4_fhn_512^3_etd3rkds_real_1gpu"))
     return res, cfg, prob
 
 
-def sharded_subrun(args, rank, world, timeout_s=240):
+def sharded_subrun(args, rank, world, timeout_s=480):
     """N > 1 replicas runs also measure the north_star's multi-GPU workload: C4 (512^3)
     slab-sharded over the same GPUs (direct peer stores + NCCL barriers), in child processes
     with their own rendezvous and a timeout, so that a failure there cannot take the headline
@@ -663,9 +820,11 @@ def sharded_subrun(args, rank, world, timeout_s=240):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
-               MASTER_PORT=str(port[0]), LOCAL_RANK=os.environ.get("LOCAL_RANK", str(rank)))
+               MASTER_PORT=str(port[0]), LOCAL_RANK=os.environ.get("LOCAL_RANK", str(rank)),
+               NCCL_DEBUG="INFO")
+    steps = 10
     cmd = [sys.executable, os.path.abspath(__file__), "--gpus", str(world), "--config", "C4",
-           "--mode", "sharded", "--steps", "5", "--warmup", "3", "--no-extras"]
+           "--mode", "sharded", "--steps", str(steps), "--warmup", "3", "--no-extras"]
     try:
         r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout_s)
         out = {"rc": r.returncode}
@@ -674,13 +833,20 @@ def sharded_subrun(args, rank, world, timeout_s=240):
             if r.returncode == 0 and lines:
                 d = json.loads(lines[-1])
                 out = {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"],
+                       "steps": d["steps"], "warmup": d["warmup"],
                        "n_gpus": d["n_gpus"], "scaling": d["scaling"],
                        "workload": d["config"]["workload"], "parallelism": d["config"]["parallelism"],
-                       "roofline_frac": d["roofline"]["frac"], "clocks": d.get("clocks")}
+                       "exchange": d.get("exchange"), "check": d.get("check"),
+                       "roofline_frac": d["roofline"]["frac"], "clocks": d.get("clocks"),
+                       "finite": d.get("finite")}
             else:
-                out["error"] = (r.stderr.strip().splitlines() or ["no output"])[-1][:300]
+                out["error"] = [l for l in r.stderr.strip().splitlines() if "NCCL INFO" not in l][-3:]
+            # NCCL communicator evidence (NCCL_DEBUG=INFO on the child ranks)
+            info = [l.strip() for l in r.stderr.splitlines() if "NCCL INFO" in l]
+            out["nccl_comm_lines"] = [l[-160:] for l in info if "nRanks" in l][:4]
+            out["nccl_nvls_lines"] = [l[-160:] for l in info if "NVLS" in l][:3]
     except subprocess.TimeoutExpired:
-        out = {"error": f"timeout after {timeout_s} s"}
+        out = {"error": f"timeout after {timeout_s} s", "steps": steps}
     dist.barrier()
     return out if rank == 0 else None
 
@@ -749,7 +915,7 @@ def main():
     achieved = prof["gemm_flops"] / prof["gemm_ms"] / 1e9 if prof["gemm_ms"] > 0 else None
     launches = res["cnt"]["gemm_launches"] + res["cnt"]["other_launches"]
     gemm_launches = prof["gemm_launches"]
-    traffic = load_traffic(args.config)
+    traffic, traffic_alg = load_traffic(args.config)
     step_flops = res["cnt"]["mode_product_flops"] / max(1, res["cnt"]["steps"])
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
@@ -768,6 +934,10 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if (achieved and peak) else None,
                      "traffic": traffic,
+                     "traffic_alg": traffic_alg,
+                     "traffic_per": "step: the sum over all mode-product GEMM launches of one step "
+                                    "(ncu dram__bytes_read.sum + dram__bytes_write.sum; traffic_alg = each "
+                                    "operand read once, the output written once)",
                      "peak_source": peak_src,
                      "measured_over": "a second pass of the same K steps with a CUDA-event pair "
                                       "around every kernel (event-record nodes in the step graph)",
@@ -781,6 +951,10 @@ def main():
         "phi_bank_setup_s": res["phi_s"],
         "finite": res["finite"],
     }
+    if sharded:
+        line["exchange"] = res.get("exchange")
+        if res.get("check"):
+            line["check"] = res["check"]
     if "e2e_ms" in res:
         line["e2e"] = {"value": (1 if sharded else world) * 1e3 / res["e2e_ms"], "unit": "steps/s",
                        "h2d_bytes_per_step": res["e2e_bytes"], "d2h_bytes_per_step": res["e2e_bytes"]}
@@ -791,6 +965,8 @@ def main():
         line["tucker_batched_tflops"] = tk["batched"]
         line["tucker_batch_size"] = tk["batch"]
         line["other_workloads"] = res.get("others")
+        if res.get("f32"):
+            line["fp32_variant"] = res["f32"]
         if res.get("emulated"):
             line["sharded_c4_emulated"] = res["emulated"]
         if peak:
@@ -804,6 +980,12 @@ def main():
         line["cpu_baseline_1core"] = {"value": v1, "unit": "steps/s", "cores": 1, "kind": "oracle",
                                       "sample": sample1}
     if extra_sharded is not None:
+        c4 = (res.get("others") or {}).get("C4_fhn_512^3_etd3rkds_real_1gpu") or {}
+        if extra_sharded.get("ms_per_step") and c4.get("ms_per_step"):
+            P = extra_sharded["n_gpus"]
+            extra_sharded["one_gpu_ms_per_step"] = c4["ms_per_step"]
+            extra_sharded["parallel_efficiency"] = round(c4["ms_per_step"] / (P * extra_sharded["ms_per_step"]), 4)
+            extra_sharded["efficiency_def"] = "E(P) = T(1 GPU) / (P T(P)), C4 512^3 step, both measured in this job"
         line["sharded_c4"] = extra_sharded
     print(json.dumps(line))
     if world > 1:

@@ -1,9 +1,9 @@
 """Paper-protocol convergence on the GPU (Figs. 1/4/5/8):
 absolute inf-norm error over both species against a reference exprk3ds_real run with many
 steps ("a sufficiently large number of time steps"), at the paper's grids, final
-times and step ladders; prints one JSON object (errors, fitted slopes, steps/s).
+times and step ladders (Figs. 1/4/5/8); prints one JSON object (errors, fitted slopes, steps/s).
 
-    python tools/convergence.py [--quick] > profiles/convergence_r01.json
+    python tools/convergence.py [--quick] [--only fig8] > profiles/convergence_r02.json
 """
 import json
 import os
@@ -58,6 +58,13 @@ PROTOCOLS = [
       "etd2rkds": [2.253e-4, 1.920e-4, 1.655e-4, 1.442e-4],
       "exprk3ds_real": [9.054e-5, 5.997e-5, 4.151e-5, 2.970e-5],
       "exprk3ds_cplx": [9.110e-5, 6.035e-5, 4.177e-5, 2.990e-5]}),
+    ("fig8_fhn_n100_T5", "fhn", 3, 100, 5.0, 100000,
+     {"etd2rkds": [60000, 65000, 70000, 75000], "exprk3ds_real": [14000, 16000, 18000, 20000],
+      "exprk3ds_cplx": [14000, 16000, 18000, 20000]},
+     {"source": "P:1919-1925 (protocol), P:1953-2001 (Fig. 8 data, CUDA double, n = 100)",
+      "etd2rkds": [5.012e-4, 4.270e-4, 3.682e-4, 3.207e-4],
+      "exprk3ds_real": [2.107e-4, 1.378e-4, 9.534e-5, 6.823e-5],
+      "exprk3ds_cplx": [2.085e-4, 1.381e-4, 9.557e-5, 6.840e-5]}),
 ]
 
 
