@@ -579,7 +579,7 @@ def emulate_sharded_p8(kx, torch, stream, c4_one, P=8, steps=3, warm=2):
     return out
 
 
-def sharded_closed_form_check(kx, torch, stream, cfg, n, rank, world, uid, p2p, dist):
+def sharded_closed_form_check(kx, torch, stream, cfg, n, rank, world, dist):
     """Correctness of the sharded step at full size, without an oracle run: g = 0 and cosine-mode
     data (an eigenvector of every Neumann Laplacian A_mu, inputs.cosine_mode) make one exprk3ds
     step the scalar recurrence U+ = Re(1 + tau sum_mu lam_mu sum_i eta_i prod_mu
@@ -600,7 +600,10 @@ def sharded_closed_form_check(kx, torch, stream, cfg, n, rank, world, uid, p2p, 
     ndl = n[-1] // world
     modes[-1] = modes[-1][rank * ndl:(rank + 1) * ndl]          # this rank's i_d block
     x = inputs.kron_vec(modes)
-    ctx = kx.Context(torch.cuda.current_device(), stream, dist=(uid, rank, world))
+    uid = [kx.nccl_unique_id() if rank == 0 else None]   # a fresh communicator needs a fresh id
+    if dist is not None:
+        dist.broadcast_object_list(uid, src=0)
+    ctx = kx.Context(torch.cuda.current_device(), stream, dist=(uid[0], rank, world))
     try:
         ctx.set_grid(n, 2)
         for c in range(2):
@@ -784,8 +787,8 @@ def run_kx(args, rank, world, sharded):
     if sharded and cfg["d"] == 3:   # after the timed context is gone (memory)
         del U
         torch.cuda.empty_cache()
-        res["check"] = sharded_closed_form_check(kx, torch, stream, cfg, prob.n, rank, world, uid[0],
-                                                 exchange == "p2p", dist if world > 1 else None)
+        res["check"] = sharded_closed_form_check(kx, torch, stream, cfg, prob.n, rank, world,
+                                                 dist if world > 1 else None)
     if not args.no_extras and rank == 0 and not sharded:
         del U, flush
         torch.cuda.empty_cache()
