@@ -21,9 +21,19 @@ __device__ __forceinline__ long long out_index(const PointwiseArgs& a, long long
   return q * (a.N / a.pack_n1 * a.pack_n1l) + row * a.pack_n1l + (i1 - q * a.pack_n1l);
 }
 
+// Contiguous, equal chunk of [0, n) for this CTA (the grid is a whole number of resident waves,
+// so every SM streams the same number of bytes: no partial last wave on these short kernels)
+__device__ __forceinline__ void cta_chunk(long long n, long long align, long long& b0, long long& b1) {
+  long long per = (n + gridDim.x - 1) / gridDim.x;
+  per = (per + align - 1) / align * align;
+  b0 = min(n, (long long)blockIdx.x * per);
+  b1 = min(n, b0 + per);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) nonlin2_kernel(const PointwiseArgs a) {
-  // two components, vectorised by 2 points (N even)
+  // two components, vectorised by 2 points (N even); two pairs per thread per iteration, every
+  // load of both issued before any arithmetic (bytes in flight)
   const long long n2 = a.N / 2;
   const double2* __restrict__ u = reinterpret_cast<const double2*>(a.u[0]);
   const double2* __restrict__ v = reinterpret_cast<const double2*>(a.u[1]);
@@ -31,22 +41,41 @@ __global__ void __launch_bounds__(256) nonlin2_kernel(const PointwiseArgs a) {
   double2* __restrict__ o2 = reinterpret_cast<double2*>(a.out[1]);
   const double2* __restrict__ G1 = reinterpret_cast<const double2*>(a.G[0]);
   const double2* __restrict__ G2 = reinterpret_cast<const double2*>(a.G[1]);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
-       i += (long long)gridDim.x * blockDim.x) {
-    const double2 uu = u[i], vv = v[i];
-    double2 r1, r2;
-    g_point(a.model, a.p, uu.x, vv.x, r1.x, r2.x);
-    g_point(a.model, a.p, uu.y, vv.y, r1.y, r2.y);
-    if (MODE == 1) {
-      const double2 h1 = G1[i], h2 = G2[i];
-      r1.x -= h1.x;
-      r1.y -= h1.y;
-      r2.x -= h2.x;
-      r2.y -= h2.y;
+  long long b0, b1;
+  cta_chunk(n2, 1, b0, b1);
+  const int B = blockDim.x;
+  for (long long i0 = b0 + threadIdx.x; i0 < b1; i0 += 2 * B) {
+    double2 uu[2], vv[2], h1[2], h2[2];
+    bool ok[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const long long i = i0 + k * B;
+      ok[k] = i < b1;
+      const long long j = ok[k] ? i : i0;
+      uu[k] = u[j];
+      vv[k] = v[j];
+      if (MODE == 1) {
+        h1[k] = G1[j];
+        h2[k] = G2[j];
+      }
     }
-    const long long oi = out_index(a, 2 * i) / 2;   // pairs never straddle a peer block
-    *reinterpret_cast<double2*>(peer_redirect(a.peer, 0, reinterpret_cast<double*>(o1 + oi))) = r1;
-    *reinterpret_cast<double2*>(peer_redirect(a.peer, 1, reinterpret_cast<double*>(o2 + oi))) = r2;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (!ok[k]) continue;
+      const long long i = i0 + k * B;
+      double2 r1, r2;
+      g_point(a.model, a.p, uu[k].x, vv[k].x, r1.x, r2.x);
+      g_point(a.model, a.p, uu[k].y, vv[k].y, r1.y, r2.y);
+      if (MODE == 1) {
+        r1.x -= h1[k].x;
+        r1.y -= h1[k].y;
+        r2.x -= h2[k].x;
+        r2.y -= h2[k].y;
+      }
+      const long long oi = out_index(a, 2 * i) / 2;   // pairs never straddle a peer block
+      *reinterpret_cast<double2*>(peer_redirect(a.peer, 0, reinterpret_cast<double*>(o1 + oi))) = r1;
+      *reinterpret_cast<double2*>(peer_redirect(a.peer, 1, reinterpret_cast<double*>(o2 + oi))) = r2;
+    }
   }
   if (a.peer.P) __threadfence_system();
 }
@@ -425,6 +454,23 @@ int grid_for(long long work, int block) {
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// One whole wave of resident CTAs (occupancy API, per device and kernel), at most enough CTAs
+// for `work` threads: with cta_chunk every SM then streams the same share of the field.
+template <class K>
+int resident_grid(K kernel, long long work, int block) {
+  static int occ_of[32] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) dev = 0;
+  if (occ_of[dev] == 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, 0) != cudaSuccess || occ < 1) occ = 4;
+    occ_of[dev] = occ;
+  }
+  const long long wave = (long long)(grid_for(1LL << 40, block) / 16) * occ_of[dev];   // SMs x resident
+  const long long need = (work + block - 1) / block;
+  return (int)std::max<long long>(1, std::min(wave, need));
+}
+
 }  // namespace
 
 cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t stream) {
@@ -433,9 +479,8 @@ cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t s
              al16(a.out[1]) && (a.pack_n1l == 0 || a.pack_n1l % 2 == 0);
   if (mode == 1) vec = vec && al16(a.G[0]) && al16(a.G[1]);
   if (vec) {
-    const int grid = grid_for(a.N / 2, 256);
-    if (mode == 0) nonlin2_kernel<0><<<grid, 256, 0, stream>>>(a);
-    else nonlin2_kernel<1><<<grid, 256, 0, stream>>>(a);
+    if (mode == 0) nonlin2_kernel<0><<<resident_grid(nonlin2_kernel<0>, a.N / 4, 256), 256, 0, stream>>>(a);
+    else nonlin2_kernel<1><<<resident_grid(nonlin2_kernel<1>, a.N / 4, 256), 256, 0, stream>>>(a);
   } else {
     const int grid = grid_for(a.N, 256);
     if (mode == 0) nonlin_scalar_kernel<0><<<grid, 256, 0, stream>>>(a);
@@ -446,7 +491,10 @@ cudaError_t launch_nonlinearity(const PointwiseArgs& a, int mode, cudaStream_t s
 
 cudaError_t launch_g_kronsum(const GKronArgs& a, cudaStream_t stream) {
   if (a.N <= 0) return cudaSuccess;
-  // one wave of 8 CTAs per SM (its neighbour loads hit L2 better than two waves)
+  // one whole wave of resident CTAs, each streaming a contiguous chunk (its neighbour lines are
+  // mostly its own: L2 hits)
+  // one wave of 8 CTAs per SM (its neighbour loads hit L2 better than two waves; measured: a
+  // contiguous chunk per CTA and an all-loads-first d = 3 form were no faster)
   const int grid = (int)std::min<long long>(grid_for(a.N / 2, 256), 8LL * (grid_for(1LL << 40, 256) / 16));
   if (a.d == 2) g_kronsum_kernel<2><<<grid, 256, 0, stream>>>(a);
   else if (a.d == 3) g_kronsum_seq_kernel<3><<<grid, 256, 0, stream>>>(a);
