@@ -260,6 +260,14 @@ struct GemmTile {
 
     __device__ __forceinline__ void issue(const GemmArgs& p, double* as, double* bs) {
       const int tid = threadIdx.x;
+      if (p.diag_noload) {   // diagnostics: the pipeline without its copies
+        lk0 += BK;
+        if (lk0 >= p.kseg) {
+          lk0 = 0;
+          ++lseg;
+        }
+        return;
+      }
       const int kseg = p.kseg;
       const double* Ab = A + p.seg_off[lseg] + (AROW ? (long long)lk0 : (long long)lk0 * p.lda);
       const double* Bb = B + ((long long)lseg * kseg + lk0) * p.ldb;
@@ -945,6 +953,8 @@ double gemm_flops(const GemmArgs& g) {
 
 cudaError_t launch_gemm(const GemmArgs& g_in, cudaStream_t stream) {
   GemmArgs g = g_in;
+  static const int noload = getenv("KX_GEMM_NOLOAD") ? 1 : 0;   // diagnostics only
+  g.diag_noload = noload;
   // batched COL-layout launches (middle modes) with ragged N: one launch over nb * N columns
   // instead of nb launches' worth of padded tiles (the paper's n = 100, 150, 200)
   g.nflat = 0;

@@ -63,6 +63,7 @@ struct GemmArgs {
   // of the tile width are run as one launch over N' = nb N columns; column n' is batch
   // n' / nflat, column n' % nflat (the B/C/D/E batch strides apply per column)
   int nflat = 0;
+  int diag_noload = 0;   // diagnostics only (KX_GEMM_NOLOAD=1): skip the operand copies (wrong results)
 };
 constexpr int kSkSlots = 304;    // partial-tile slots of 128x128 doubles (>= 2 x SM count)
 constexpr int kSkFlags = 2048;   // counters: a pair per split tile
