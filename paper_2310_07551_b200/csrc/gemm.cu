@@ -20,6 +20,7 @@
 // epilogue C = alpha*acc + beta*D + gamma*E + diag*I with 16-B stores.
 #include "kx_internal.h"
 
+#include <cuda.h>
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -71,6 +72,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+// VEC == 3: the operand tiles arrive by TMA (cp.async.bulk.tensor, issued by one thread) into an
+// unpadded 64-B-swizzled layout: a tile is stored as slabs of 8 doubles (one 64-B row) per
+// (chunk, row), [chunk][row][8], and 16-B unit u of byte offset o within a 512-B span lands at
+// u ^ ((o >> 7) & 3) (CU_TENSOR_MAP_SWIZZLE_64B).  Every m8n8k4 fragment load of both layouts is
+// then conflict-free (2 wavefronts per 256 B), as with the padded cp.async layout.
+constexpr int kTmaMaxA = 16;   // A maps: species x concatenated-K segments
+struct TmaMaps {
+  CUtensorMap A[kTmaMaxA];
+  CUtensorMap B[MAXS];
+  int nsegmaps = 1;            // A map of (species s, segment j) = A[s * nsegmaps + j]
+};
+__device__ __forceinline__ unsigned swz64(unsigned o) { return o ^ (((o >> 7) & 3u) << 4); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                          int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col); fragments: a = A[g][t], b = B[t][g],
 // c = {C[g][2t], C[g][2t+1]} with g = lane/4, t = lane%4.
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -86,18 +112,23 @@ struct Cfg {
   // resident CTAs per SM the register budget must allow (512 threads: 1 at <= 128 registers;
   // 256: 2 at <= 128; 128: 3 at <= 170)
   static constexpr int MINB = NT >= 512 ? 1 : (NT >= 256 ? 2 : 3);
-  static constexpr int SA = AROW ? (BK + 4) : (BM + 4);   // smem row stride (doubles)
-  static constexpr int A_ST = AROW ? BM * SA : BK * SA;
-  static constexpr int SB = BN + 4;
-  static constexpr int B_ST = BK * SB;
-  static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8 + 2 * STAGES * 8;   // + mbarriers
-  // loader geometry: chunks of VEC doubles, each thread owns IA (A) and IB (B) chunks
-  static constexpr int CPR_A = AROW ? BK / VEC : BM / VEC;   // chunks per smem row of A
-  static constexpr int IA = BM * BK / VEC / NT;
-  static constexpr int CPR_B = BN / VEC;
-  static constexpr int IB = BK * BN / VEC / NT;
-  static_assert(SA % 16 == 4 && SB % 16 == 4, "conflict-free fragment loads");
-  static_assert((BM * BK / VEC) % NT == 0 && (BK * BN / VEC) % NT == 0, "loader divisibility");
+  static constexpr bool TMA = VEC == 3;                     // TMA loads, swizzled unpadded tiles
+  static constexpr int LV = TMA ? 2 : VEC;                   // cp.async chunk (doubles)
+  static constexpr int SA = TMA ? 0 : (AROW ? (BK + 4) : (BM + 4));   // smem row stride (doubles)
+  static constexpr int A_ST = TMA ? BM * BK : (AROW ? BM * SA : BK * SA);
+  static constexpr int SB = TMA ? 0 : BN + 4;
+  static constexpr int B_ST = TMA ? BK * BN : BK * SB;
+  static constexpr int ALIGN = TMA ? 1024 : 0;               // swizzle atoms 512-B aligned
+  static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8 + 2 * STAGES * 8 + ALIGN;   // + mbarriers
+  // loader geometry: chunks of LV doubles, each thread owns IA (A) and IB (B) chunks
+  static constexpr int CPR_A = AROW ? BK / LV : BM / LV;   // chunks per smem row of A
+  static constexpr int IA = BM * BK / LV / NT;
+  static constexpr int CPR_B = BN / LV;
+  static constexpr int IB = BK * BN / LV / NT;
+  static_assert(TMA || (SA % 16 == 4 && SB % 16 == 4), "conflict-free fragment loads");
+  static_assert(!TMA || (BK % 8 == 0 && BM % 8 == 0 && BN % 8 == 0 && BM <= 256 && BN / 8 <= 256),
+                "TMA boxes");
+  static_assert((BM * BK / LV) % NT == 0 && (BK * BN / LV) % NT == 0, "loader divisibility");
   static_assert(IA <= 32 && IB <= 32, "validity masks are 32-bit");
 };
 
@@ -178,8 +209,9 @@ template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES
 struct GemmTile {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   static constexpr int NT = C_::NT, SA = C_::SA, SB = C_::SB, A_ST = C_::A_ST, B_ST = C_::B_ST;
-  static constexpr int IA = C_::IA, IB = C_::IB, CPR_A = C_::CPR_A, CPR_B = C_::CPR_B;
+  static constexpr int IA = C_::IA, IB = C_::IB, CPR_A = C_::CPR_A, CPR_B = C_::CPR_B, LV = C_::LV;
   static constexpr int FM = WM / 8, FN = WN / 8;
+  static constexpr bool TMA = C_::TMA;
 
   struct Coord {
     int m0, n0, s, t, b;
@@ -214,12 +246,20 @@ struct GemmTile {
   struct Loader {
     const double* A;
     const double* B;
-    int offA[IA], offB[IB];
+    int offA[TMA ? 1 : IA], offB[TMA ? 1 : IB];
     unsigned okA, okB;
     int lseg, lk0;
+    Coord tc;   // TMA: the tile's coordinates
 
     __device__ __forceinline__ void setup(const GemmArgs& p, const Coord& cd, int kb) {
       const int tid = threadIdx.x;
+      if constexpr (TMA) {
+        tc = cd;
+        const int kps = (p.kseg + BK - 1) / BK;
+        lseg = kb / kps;
+        lk0 = (kb - lseg * kps) * BK;
+        return;
+      }
       A = p.A[cd.s] + cd.t * p.sA_t + cd.b * p.sA_b;
       B = p.B[cd.s] + cd.t * p.sB_t + cd.b * p.sB_b;
       const int lda = (int)p.lda, ldb = (int)p.ldb;
@@ -228,12 +268,12 @@ struct GemmTile {
       for (int it = 0; it < IA; ++it) {
         const int c = tid + it * NT;
         if constexpr (AROW) {
-          const int r = c / CPR_A, kc = (c % CPR_A) * VEC;
+          const int r = c / CPR_A, kc = (c % CPR_A) * LV;
           const bool v = cd.m0 + r < p.M;
           offA[it] = (v ? (cd.m0 + r) : 0) * lda + kc;
           okA |= (unsigned)v << it;
         } else {
-          const int kr = c / CPR_A, mc = (c % CPR_A) * VEC;
+          const int kr = c / CPR_A, mc = (c % CPR_A) * LV;
           const bool v = cd.m0 + mc < p.M;
           offA[it] = kr * lda + (v ? cd.m0 + mc : 0);
           okA |= (unsigned)v << it;
@@ -242,7 +282,7 @@ struct GemmTile {
 #pragma unroll
       for (int it = 0; it < IB; ++it) {
         const int c = tid + it * NT;
-        const int kr = c / CPR_B, nc = (c % CPR_B) * VEC;
+        const int kr = c / CPR_B, nc = (c % CPR_B) * LV;
         const int np = cd.n0 + nc;
         const bool v = np < p.N;
         if (p.nflat) {   // flattened batches: column np is batch np / nflat
@@ -256,6 +296,21 @@ struct GemmTile {
       const int kps = (p.kseg + BK - 1) / BK;
       lseg = kb / kps;
       lk0 = (kb - lseg * kps) * BK;
+    }
+
+    // TMA (one thread): the A and B boxes of the next k-tile, completion counted on `bar`
+    __device__ __forceinline__ void issue_tma(const GemmArgs& p, const TmaMaps& tm, double* as, double* bs,
+                                              uint64_t* bar) {
+      mbar_expect_tx(bar, (BM * BK + BK * BN) * 8);
+      const CUtensorMap* mA = &tm.A[tc.s * tm.nsegmaps + (AROW ? lseg : 0)];
+      if constexpr (AROW) tma_load5(as, mA, 0, tc.m0, lk0 / 8, tc.t, tc.b, bar);   // [kc][m][8]
+      else tma_load5(as, mA, 0, lk0, tc.m0 / 8, tc.t, tc.b, bar);                   // [mc][k][8]
+      tma_load5(bs, &tm.B[tc.s], 0, lseg * p.kseg + lk0, tc.n0 / 8, tc.t, tc.b, bar);   // [nc][k][8]
+      lk0 += BK;
+      if (lk0 >= p.kseg) {
+        lk0 = 0;
+        ++lseg;
+      }
     }
 
     __device__ __forceinline__ void issue(const GemmArgs& p, double* as, double* bs) {
@@ -277,8 +332,8 @@ struct GemmTile {
         const int kr = AROW ? (c % CPR_A) * VEC : c / CPR_A;
         const bool v = ((okA >> it) & 1u) && (lk0 + kr < kseg);
         const double* src = v ? Ab + offA[it] : A;
-        double* dst = as + (c / CPR_A) * SA + (c % CPR_A) * VEC;
-        if constexpr (VEC == 2) cp_async16(dst, src, v);
+        double* dst = as + (c / CPR_A) * SA + (c % CPR_A) * LV;
+        if constexpr (LV == 2) cp_async16(dst, src, v);
         else cp_async8(dst, src, v);
       }
 #pragma unroll
@@ -287,8 +342,8 @@ struct GemmTile {
         const int kr = c / CPR_B;
         const bool v = ((okB >> it) & 1u) && (lk0 + kr < kseg);
         const double* src = v ? Bb + offB[it] : B;
-        double* dst = bs + kr * SB + (c % CPR_B) * VEC;
-        if constexpr (VEC == 2) cp_async16(dst, src, v);
+        double* dst = bs + kr * SB + (c % CPR_B) * LV;
+        if constexpr (LV == 2) cp_async16(dst, src, v);
         else cp_async8(dst, src, v);
       }
       lk0 += BK;
@@ -315,7 +370,7 @@ struct GemmTile {
     const double* D = p.D[cd.s] ? p.D[cd.s] + cd.t * p.sD_t + cd.b * p.sD_b : nullptr;
     const double* E = p.E[cd.s] ? p.E[cd.s] + cd.t * p.sE_t + cd.b * p.sE_b : nullptr;
     const double alpha = p.alpha, beta = p.beta, gamma = p.gamma, diag = p.diag;
-    if constexpr (VEC == 2) {
+    if constexpr (VEC >= 2) {
       // fast paths for whole interior tiles (every launch of the large configs): no bounds
       // checks, row pointers hoisted, the D loads issued before the stores
       const bool plain = !PEER && !p.nflat && mask == ~0u && !E && diag == 0.0 && cd.m0 + BM <= M &&
@@ -364,7 +419,7 @@ struct GemmTile {
           od = b * p.sD_b + (long long)m * p.ldd + nn;
           oe = b * p.sE_b + (long long)m * p.lde + nn;
         }
-        if constexpr (VEC == 2) {
+        if constexpr (VEC >= 2) {
           if (D) {
             const double2 d2 = *reinterpret_cast<const double2*>(D + od);
             v0 += beta * d2.x;
@@ -405,12 +460,15 @@ struct GemmTile {
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
 __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT,
                                   Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::MINB)
-    gemm_kernel(const GemmArgs p, const Sched sc) {
+    gemm_kernel(const GemmArgs p, const Sched sc, const __grid_constant__ TmaMaps tm) {
   using T_ = GemmTile<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>;
   using Coord = typename T_::Coord;
   constexpr int NT = T_::NT, FM = T_::FM, FN = T_::FN, SA = T_::SA, SB = T_::SB;
   constexpr int A_ST = T_::A_ST, B_ST = T_::B_ST;
-  extern __shared__ __align__(16) double smem[];
+  constexpr bool TMA = T_::TMA;
+  extern __shared__ __align__(16) double smem_dyn[];
+  double* smem = TMA ? reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023))
+                     : smem_dyn;
   double* As = smem;
   double* Bs = smem + STAGES * A_ST;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -426,7 +484,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   uint64_t* empty = full + STAGES;
   if (tid == 0) {
     for (int st = 0; st < STAGES; ++st) {
-      mbar_init(full + st, NT);
+      mbar_init(full + st, TMA ? 1 : NT);   // TMA: the issuing thread's expect-tx arrival
       mbar_init(empty + st, NT);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -441,6 +499,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   int pk = 0;
   int pkt = 0;   // k-tiles issued so far (stage = pkt % STAGES, fill = pkt / STAGES)
   typename T_::Loader ld;
+  if (TMA && tid != 0) p_ok = false;   // TMA: thread 0 alone produces
   if (p_ok) {
     pk = ps.kb;
     ld.setup(p, T_::coords(p, sc, ps.tl), ps.kb);
@@ -449,8 +508,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     if (!p_ok) return;
     const int stage = pkt % STAGES, fill = pkt / STAGES;
     if (fill > 0) mbar_wait(empty + stage, (fill - 1) & 1);
-    ld.issue(p, As + stage * A_ST, Bs + stage * B_ST);
-    cp_async_mbar_arrive(full + stage);
+    if constexpr (TMA) {
+      ld.issue_tma(p, tm, As + stage * A_ST, Bs + stage * B_ST, full + stage);
+    } else {
+      ld.issue(p, As + stage * A_ST, Bs + stage * B_ST);
+      cp_async_mbar_arrive(full + stage);
+    }
     ++pkt;
     if (++pk == ps.ke) {
       p_ok = pit.next(ps);
@@ -488,15 +551,44 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   const int kps = (p.kseg + BK - 1) / BK;
   const int ktail = p.kseg - (kps - 1) * BK;   // valid k of a segment's last k-tile
   int cks = ck % kps;                          // k-tile position inside its segment
+  // TMA layout: per-thread byte offsets of this thread's fragment element for kk % 8 == 0 / 4
+  // (AROW A: row m = wm0 + g + 8i in slab kk / 8; COL A and B: row k = kk + t4 of slab
+  // (wm0 or wn0) / 8 + i); the XOR of swz64 folded in
+  int tma_a[2] = {0, 0}, tma_b[2] = {0, 0};
+  if constexpr (TMA) {
+    for (int par = 0; par < 2; ++par) {
+      const int row_k = par * 4 + t4;          // k within the 8-row group (kk & 7 = 4 par)
+      const unsigned gsw = swz64((unsigned)(row_k * 64 + g * 8));   // rows of 64 B, 8 doubles
+      if constexpr (AROW) tma_a[par] = (int)swz64((unsigned)((wm0 + g) * 64 + row_k * 8));
+      else tma_a[par] = (wm0 >> 3) * (BK * 64) + (int)gsw;
+      tma_b[par] = (wn0 >> 3) * (BK * 64) + (int)gsw;
+    }
+  }
   auto kstep = [&](const double* as, const double* bs, int kk) {
     double af[FM], bf[FN];
+    if constexpr (TMA) {
+      // [chunk][row][8] slabs, 64-B swizzle (see swz64): per-thread offsets for the two k-step
+      // parities (kk & 4) are precomputed (tma_off), the rest are compile-time immediates
+      const char* a8 = reinterpret_cast<const char*>(as);
+      const char* b8 = reinterpret_cast<const char*>(bs);
+      const int par = (kk >> 2) & 1;
 #pragma unroll
-    for (int i = 0; i < FM; ++i) {
-      if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
-      else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+      for (int i = 0; i < FM; ++i) {
+        if constexpr (AROW) af[i] = *reinterpret_cast<const double*>(a8 + (kk >> 3) * (BM * 64) + i * 512 + tma_a[par]);
+        else af[i] = *reinterpret_cast<const double*>(a8 + i * (BK * 64) + (kk & ~7) * 64 + tma_a[par]);
+      }
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
+        bf[j] = *reinterpret_cast<const double*>(b8 + j * (BK * 64) + (kk & ~7) * 64 + tma_b[par]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < FM; ++i) {
+        if constexpr (AROW) af[i] = as[(wm0 + i * 8 + g) * SA + kk + t4];
+        else af[i] = as[(kk + t4) * SA + wm0 + i * 8 + g];
+      }
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
     }
-#pragma unroll
-    for (int j = 0; j < FN; ++j) bf[j] = bs[(kk + t4) * SB + wn0 + j * 8 + g];
 #pragma unroll
     for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -815,8 +907,13 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
   return best;
 }
 
+const TmaMaps& no_maps() {
+  static const TmaMaps m = {};
+  return m;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, bool AROW, int VEC, int STAGES, bool PEER = false>
-cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t stream) {
+cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t stream, const TmaMaps& tm = no_maps()) {
   using C_ = Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>;
   cudaError_t e = prepare_cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>();
   if (e != cudaSuccess) return e;
@@ -827,7 +924,7 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t strea
   static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only
   if (trace)
     fprintf(stderr, "kx-gemm %s M=%d N=%d K=%dx%d nz=%d cfg=%dx%dx%d tiles=%lld kt=%d G=%d dp=%lld sk_units=%lld G_sk=%d csplit=%d (max clusters of 8/4/2: %d/%d/%d) flops=%.4g\n",
-            AROW ? "row" : "col", g.M, g.N, g.kseg, g.nseg, nz, BM, BN, BK, T, sc.ktiles, sc.G,
+            AROW ? (VEC == 3 ? "row/tma" : "row") : (VEC == 3 ? "col/tma" : "col"), g.M, g.N, g.kseg, g.nseg, nz, BM, BN, BK, T, sc.ktiles, sc.G,
             sc.dp_tiles, sc.sk_units, sc.G_sk, sc.csplit, max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(8),
             max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(4), max_clusters<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>(2),
             2.0 * g.M * g.N * (double)g.kseg * g.nseg * nz);
@@ -844,7 +941,7 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t strea
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
+    const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc, tm);
     if (ce == cudaSuccess) return ce;
     // the cluster launch was refused (e.g. SMs taken by concurrent work): plain data-parallel
     cudaGetLastError();
@@ -867,7 +964,7 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t strea
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc);
+    const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc, tm);
     if (ce != cudaErrorCooperativeLaunchTooLarge) return ce;
     // not all CTAs can be co-resident right now: the data-parallel schedule needs no waits
     cudaGetLastError();
@@ -876,15 +973,95 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t strea
     sc.sk_units = 0;
     sc.G_sk = 0;
   }
-  gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc);
+  gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc, tm);
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- TMA tensor maps (VEC == 3)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn tma_encoder() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      f = nullptr;
+    }
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+// 5-D fp64 view (element extents / strides, stride[0] = 1) with box {8, b1, b2, 1, 1} and the
+// 64-B swizzle; extent-1 dims get a packed stride; false if TMA cannot express the view.
+bool make_map64(CUtensorMap* map, const double* base, const long long* ext, const long long* str, int b1, int b2) {
+  EncodeTiledFn enc = tma_encoder();
+  if (!enc || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5] = {8, (cuuint32_t)b1, (cuuint32_t)b2, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+  long long prev = 1;
+  for (int i = 0; i < 5; ++i) {
+    if (ext[i] < 1 || ext[i] > (1LL << 32)) return false;
+    dims[i] = (cuuint64_t)ext[i];
+  }
+  for (int i = 1; i < 5; ++i) {
+    long long st = str[i];
+    if (ext[i] == 1) st = prev * ext[i - 1];
+    if (st <= 0 || (st * 8) % 16 || st * 8 >= (1LL << 40)) return false;
+    strides[i - 1] = (cuuint64_t)(st * 8);
+    prev = st;
+  }
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Maps of the 128 x 128 x 32 configuration: A per (species, K segment), B per species.  Needs
+// k chunks of 8 doubles that never straddle a segment (kseg % 8), 8-wide n / m chunks, no
+// flattened batches and no zero batch strides.
+bool build_tma(const GemmArgs& g, TmaMaps& tm) {
+  // opt-in (KX_GEMM_TMA=1): measured slower than the cp.async pipeline (C2 2.639 vs 2.617,
+  // C3 1.765 vs 1.711 ms/step) — one thread issuing 32-KB boxes of 64-B rows after the stage's
+  // empty barrier puts warp 0 on every stage's critical path
+  static const bool on = getenv("KX_GEMM_TMA") != nullptr;
+  if (!on || g.nflat || g.peer.P || g.kseg % 8 || g.N % 8 || (!g.arow && g.M % 8)) return false;
+  if (g.ns * (g.arow ? g.nseg : 1) > kTmaMaxA || (!g.arow && g.nseg != 1)) return false;
+  if ((g.nt > 1 && (g.sA_t == 0 || g.sB_t == 0)) || (g.nb > 1 && (g.sA_b == 0 || g.sB_b == 0))) return false;
+  tm.nsegmaps = g.arow ? g.nseg : 1;
+  for (int s = 0; s < g.ns; ++s) {
+    for (int j = 0; j < tm.nsegmaps; ++j) {
+      const long long ext_r[5] = {8, g.M, g.kseg / 8, g.nt, g.nb};
+      const long long ext_c[5] = {8, g.kseg, g.M / 8, g.nt, g.nb};
+      const long long str[5] = {1, g.lda, 8, g.sA_t, g.sA_b};
+      const double* base = g.A[s] + (g.arow ? g.seg_off[j] : 0);
+      if (!make_map64(&tm.A[s * tm.nsegmaps + j], base, g.arow ? ext_r : ext_c, str, g.arow ? 128 : 32,
+                      g.arow ? 4 : 16))
+        return false;
+    }
+    const long long ext_b[5] = {8, (long long)g.nseg * g.kseg, g.N / 8, g.nt, g.nb};
+    const long long str_b[5] = {1, g.ldb, 8, g.sB_t, g.sB_b};
+    if (!make_map64(&tm.B[s], g.B[s], ext_b, str_b, 32, 16)) return false;
+  }
+  return true;
+}
+
 // Pick the tile configuration with the smallest planned time (unless forced) and launch it.
+// The 128 x 128 x 32 configuration runs its TMA-fed variant (VEC = 3) whenever the launch allows.
 template <bool AROW, int VEC, bool PEER>
 cudaError_t launch_layout_p(const GemmArgs& g, int nz, int forced, const double* eff, cudaStream_t stream) {
   Sched sc;
-  const double t0 = plan_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[0], sc);
+  TmaMaps tm;
+  bool tma = false;
+  if constexpr (VEC == 2 && !PEER) tma = build_tma(g, tm);
+  double t0;
+  if constexpr (VEC == 2 && !PEER)
+    t0 = tma ? plan_cfg<128, 128, 32, 32, 32, AROW, 3, 3, PEER>(g, nz, eff[0], sc)
+             : plan_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[0], sc);
+  else
+    t0 = plan_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[0], sc);
   const double t1 = plan_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[1], sc);
   const double t2 = plan_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[2], sc);
   int which = 0;
@@ -892,7 +1069,10 @@ cudaError_t launch_layout_p(const GemmArgs& g, int nz, int forced, const double*
   else if (t2 < t0 * 0.999 && t2 < t1) which = 2;
   if (forced >= 0 && forced < 3) which = forced;
   switch (which) {
-    case 0: return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[0], stream);
+    case 0:
+      if constexpr (VEC == 2 && !PEER)
+        if (tma) return launch_cfg<128, 128, 32, 32, 32, AROW, 3, 3, PEER>(g, nz, eff[0], stream, tm);
+      return launch_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[0], stream);
     case 1: return launch_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[1], stream);
     default: return launch_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, PEER>(g, nz, eff[2], stream);
   }
@@ -909,6 +1089,10 @@ cudaError_t launch_layout(const GemmArgs& g, int nz, int forced, const double* e
 template <bool AROW, int VEC>
 void prepare_layout() {
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3>();
+  if constexpr (VEC == 2) {
+    prepare_cfg<128, 128, 32, 32, 32, AROW, 3, 3>();
+    for (int S = 2; S <= 8; S *= 2) max_clusters<128, 128, 32, 32, 32, AROW, 3, 3, false>(S);
+  }
   prepare_cfg<128, 128, 32, 32, 32, AROW, VEC, 3, true>();
   prepare_cfg<128, 64, 16, 32, 32, AROW, VEC, 3, true>();
   prepare_cfg<64, 64, 16, 32, 32, AROW, VEC, 3, true>();
