@@ -51,11 +51,16 @@ def test_sm100a_only(sass):
 def test_mode_product_gemm_uses_fp64_tensor_cores(sass):
     gemms = _functions(sass, r"11gemm_kernelI")   # the fp64 template (not the tf32 kernel)
     assert len(gemms) >= 12          # 3 tile configs x 2 layouts x 2 vector widths (+ peer stores)
+    tma = _functions(sass, r"11gemm_kernelILi128ELi128ELi32ELi32ELi32ELb[01]ELi3E")   # VEC = 3
+    assert len(tma) == 2             # the opt-in TMA-fed 128x128x32 variant, both layouts
     for f in gemms:
         assert "DMMA.8x8x4" in f      # fp64 tensor-core MMA
-        assert "LDGSTS" in f          # cp.async shared-memory pipeline
         assert "SYNCS" in f           # mbarrier full/empty pipeline
         assert "HMMA" not in f
+        if f in tma:
+            assert "UTMALDG" in f and "LDGSTS" not in f   # tensor-map loads, no cp.async
+        else:
+            assert "LDGSTS" in f      # cp.async shared-memory pipeline
     # the cluster split-K path: thread-block cluster barriers in the GEMM
     assert any("UCGABAR" in f for f in gemms)
 
