@@ -163,3 +163,25 @@ def test_nccl_one_rank_operators(kx):
         assert relerr(Yd.cpu().numpy(), vec(mode_product(unvec(x, n), Ls[mu - 1], mu))) <= 1e-12
     d.close()
     one.close()
+
+
+def test_group_ops_no_out_of_bounds_writes(kx):
+    """Guard bands around every rank's output slab: the distributed operators' pack, exchange
+    copies, concat-K GEMM over source-rank segments and unpack stay inside the slabs."""
+    n, P, G = [36, 20, 16], 2, 512
+    N = int(np.prod(n))
+    Nl = N // P
+    g = make_group(kx, n, P)
+    x = inputs.uniform_sym(71, 0, N)
+    Ls = [dmat(inputs.uniform_sym(72, mu, m * m).reshape(m, m)) for mu, m in enumerate(n)]
+    bigs = [torch.full((Nl + 2 * G,), 4321.0, dtype=torch.float64, device="cuda") for _ in range(P)]
+    Ys = [b[G:G + Nl] for b in bigs]
+    Xs = [dev(slab(x, n, r, P)) for r in range(P)]
+    g.tucker(Xs, Ys, Ls, 1.0, 0.5)
+    for mu in range(1, len(n) + 1):
+        g.mode_product(Xs, Ys, mu, Ls[mu - 1], 1.0, 1.0)
+    g.ctx[0].sync()
+    for b in bigs:
+        v = b[:G].cpu().numpy().tolist() + b[G + Nl:].cpu().numpy().tolist()
+        assert len(set(v)) == 1, "guard band overwritten"
+    g.close()

@@ -190,3 +190,40 @@ def test_step_f32_full_size(kx, cfg):
     ref, tol, e32 = oracle_pair(prob, k["scheme"], k["T"], k["m"], 20)
     err = max(relerr(out[c], ref[c]) for c in range(2))
     assert err <= tol, (err, tol, e32)
+
+
+@pytest.mark.parametrize("n", [[132, 68], [36, 20, 16], [260, 4]])
+def test_f32_no_out_of_bounds_writes(kx, n):
+    """compute-sanitizer is closed on this pool: the fp32 outputs live inside larger buffers
+    whose guard bands hold a sentinel (16-B aligned offsets, as the fp32 calls require); every
+    fp32 operator and the fp32 step must leave the guards bit-identical (ragged tiles in M, N, K)."""
+    N = int(np.prod(n))
+    G = 1024
+    ctx = kx.Context(0)
+    ctx.set_grid(n, 2)
+    As = [[inputs.laplacian_neumann(m, 1.0, 1.0 + c) for m in n] for c in range(2)]
+    for c in range(2):
+        for mu in range(len(n)):
+            ctx.set_direction_matrix(c, mu + 1, As[c][mu])
+    ctx.set_model("schnakenberg" if len(n) == 2 else "fhn",
+                  inputs.SCHNAKENBERG if len(n) == 2 else inputs.FHN)
+    ctx.set_tau(1e-4, "etd3rkds")
+    X = dev32(inputs.uniform_sym(61, 0, N))
+    big = torch.full((N + 2 * G,), 12345.678, dtype=torch.float32, device="cuda")
+    Y = big[G:G + N]
+    Ls = [col32(inputs.uniform_sym(62, mu, m * m).reshape(m, m)) for mu, m in enumerate(n)]
+    ctx.tucker_f32(X, Y, Ls, 1.0, 0.5)
+    for mu in range(1, len(n) + 1):
+        ctx.mode_product_f32(X, Y, mu, Ls[mu - 1], 1.0, 1.0)
+    bigU = [torch.full((N + 2 * G,), -777.0, dtype=torch.float32, device="cuda") for _ in range(2)]
+    U = [b[G:G + N] for b in bigU]
+    for c in range(2):
+        U[c].copy_(X.abs() * 1e-3 + 1.0)
+    if len(n) in (2, 3):
+        ctx.step_f32(U, 2)
+    ctx.sync()
+    for b in [big] + bigU:
+        v = b[:G].cpu().numpy().tolist() + b[G + N:].cpu().numpy().tolist()
+        assert len(set(v)) == 1, "guard band overwritten"
+    assert all(bool(torch.isfinite(u).all()) for u in U)
+    ctx.close()

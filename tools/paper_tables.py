@@ -5,6 +5,11 @@ fp64.  Wall-clock seconds of the whole integration (phi bank included, in bracke
 paper) next to the paper's V100 "CUDA double" column.
 
     python tools/paper_tables.py [--quick]  > profiles/paper_tables_r01.json
+    python tools/paper_tables.py --f32      > profiles/paper_tables_f32_r02.json
+
+--f32: the exprk3ds_real rows in single precision (kx_step_f32, tcgen05 kind::tf32 x 3) next to
+the paper's "CUDA single" column (the grids whose extents are multiples of 4: 300^2, 600^2,
+100^3, 200^3).
 """
 import json
 import os
@@ -38,7 +43,16 @@ ROWS = [
 ]
 
 
-def run(model, d, n, T, steps, scheme):
+# (table, model, d, n, T, steps, paper V100 CUDA single seconds (phi seconds)), exprk3ds_real
+ROWS_F32 = [
+    ("Table 5", "schnakenberg", 2, 300, 2.0, 6000, (4.12, 0.26)),
+    ("Table 5", "schnakenberg", 2, 600, 2.0, 6000, (13.17, 0.51)),
+    ("Table 7", "fhn", 3, 100, 150.0, 10000, (32.59, 0.22)),
+    ("Table 7", "fhn", 3, 200, 150.0, 10000, (321.81, 0.35)),
+]
+
+
+def run(model, d, n, T, steps, scheme, f32=False):
     prob = inputs.make_problem(model, d, n, seed=0)
     ctx = kx.Context(0)
     ctx.set_grid(prob.n, 2)
@@ -46,13 +60,16 @@ def run(model, d, n, T, steps, scheme):
         for mu in range(d):
             ctx.set_direction_matrix(c, mu + 1, prob.A[c][mu])
     ctx.set_model(prob.model, prob.params)
-    U = [torch.from_numpy(u.copy()).cuda() for u in prob.U0]
+    U = [torch.from_numpy(u.astype("float32") if f32 else u.copy()).cuda() for u in prob.U0]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ctx.set_tau(T / steps, scheme)
     ctx.sync()
     t_phi = time.perf_counter() - t0
-    ctx.step_n(U, steps)
+    if f32:
+        ctx.step_f32(U, steps)   # the fp32 planes of the bank are formed by the first step
+    else:
+        ctx.step_n(U, steps)
     ctx.sync()
     total = time.perf_counter() - t0
     finite = all(bool(torch.isfinite(u).all()) for u in U)
@@ -60,7 +77,25 @@ def run(model, d, n, T, steps, scheme):
     return total, t_phi, finite
 
 
+def main_f32():
+    out = {"note": "fp32 (kx_step_f32: tcgen05 kind::tf32, three-pass split) wall-clock seconds of the "
+                   "whole exprk3ds_real integration on one B200 (phi bank in brackets) next to the "
+                   "paper's V100 CUDA single column (context, other hardware)", "rows": []}
+    for table, model, d, n, T, steps, paper in ROWS_F32:
+        total, t_phi, finite = run(model, d, n, T, steps, "etd3rkds", f32=True)
+        row = {"table": table, "model": model, "N": f"2*{n}^{d}", "T": T, "steps": steps,
+               "scheme": "etd3rkds (fp32)", "seconds": round(total, 3), "phi_seconds": round(t_phi, 3),
+               "steps_per_s": round(steps / (total - t_phi), 1), "finite": finite,
+               "paper_v100_single_seconds": paper[0], "paper_phi_seconds": paper[1],
+               "speedup_vs_paper": round(paper[0] / total, 1)}
+        out["rows"].append(row)
+        print(json.dumps(row), file=sys.stderr, flush=True)
+    print(json.dumps(out, indent=1))
+
+
 def main():
+    if "--f32" in sys.argv:
+        return main_f32()
     quick = "--quick" in sys.argv
     out = {"note": "wall-clock seconds of the whole integration on one B200 (phi bank in "
                    "brackets, as the paper's tables); the paper's column is CUDA double on a "
