@@ -33,6 +33,8 @@
 
 #include <cuda.h>
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -46,6 +48,8 @@ constexpr int T_STAGE_BYTES = 3 * T_PLANE;             // static hi, static lo, 
 constexpr int T_CONV_BYTES = 2 * T_PLANE;              // converted tensor hi, lo
 constexpr int T_SMEM = TSTAGES * T_STAGE_BYTES + TCONV * T_CONV_BYTES + 1024 /* alignment */ + 256;
 constexpr int T_THREADS = 320;
+constexpr int T_PSTRIDE = TBN + 4;                     // cluster split-K partial row (floats)
+static_assert(TBM * T_PSTRIDE * 4 <= TSTAGES * T_STAGE_BYTES, "partial fits in the stage memory");
 constexpr int T_KBUF = 4;                              // per-k-tile partial accumulators in TMEM
 constexpr int T_TMEM_COLS = T_KBUF * TBN;              // 4 x 128 fp32 columns = all of TMEM
 
@@ -126,6 +130,7 @@ __device__ __forceinline__ void split4(const float4 x, float4& h, float4& l) {
 struct Tf32GemmArgs {
   CUtensorMap mapS_hi, mapS_lo, mapT;   // 64-B aligned members first
   int kind, M, N, kseg, nseg, slo, ns, nt, nb, vec4;
+  int csplit;   // > 1: cluster split-K — the S CTAs of a cluster share one tile's k-tiles
   float alpha, beta;
   long long ldc, ldd, sC_t, sC_b, sD_t, sD_b;
   float* C[MAXS];
@@ -154,11 +159,35 @@ __device__ __forceinline__ TileCoord tile_coord(const Tf32GemmArgs& p, int tiles
   return c;
 }
 
+// Work items of a CTA: persistent over tiles (whole k range), or — cluster split-K — the one
+// tile of its cluster and its 1/S share of the k-tiles.
+template <bool SPLIT>
+struct Work {
+  int n, tl0, step, kb, ke;
+  __device__ __forceinline__ Work(const Tf32GemmArgs& p, int ntiles, int ktiles) {
+    if (SPLIT) {
+      const int r = blockIdx.x % p.csplit;
+      n = 1;
+      tl0 = blockIdx.x / p.csplit;
+      step = 1;
+      kb = r * ktiles / p.csplit;
+      ke = (r + 1) * ktiles / p.csplit;
+    } else {
+      tl0 = blockIdx.x;
+      step = gridDim.x;
+      n = tl0 < ntiles ? (ntiles - 1 - tl0) / step + 1 : 0;
+      kb = 0;
+      ke = ktiles;
+    }
+  }
+};
+
 // K-major 128-B-swizzled byte offset of element k (< 32) of row r (< 128) of a 128 x 32 tile
 __device__ __forceinline__ unsigned kmajor_off(unsigned r, unsigned kchunk) {
   return (r >> 3) * 1024 + (r & 7) * 128 + ((kchunk ^ (r & 7)) << 4);
 }
 
+template <bool SPLIT>
 __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_constant__ Tf32GemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -207,9 +236,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       int it = 0;
-      for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-        const TileCoord c = tile_coord(p, tiles_m, tiles_n, tl);
-        for (int kt = 0; kt < ktiles; ++kt, ++it) {
+      const Work<SPLIT> wk(p, ntiles, ktiles);
+      for (int w = 0; w < wk.n; ++w) {
+        const TileCoord c = tile_coord(p, tiles_m, tiles_n, wk.tl0 + w * wk.step);
+        for (int kt = wk.kb; kt < wk.ke; ++kt, ++it) {
           const int st = it % TSTAGES, fill = it / TSTAGES;
           if (fill > 0) mbar_wait(empty + st, (fill - 1) & 1);
           uint8_t* sS = smem + st * T_STAGE_BYTES;
@@ -233,8 +263,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     int it = 0;
-    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+    const Work<SPLIT> wk(p, ntiles, ktiles);
+    for (int w = 0; w < wk.n; ++w) {
+      for (int kt = wk.kb; kt < wk.ke; ++kt, ++it) {
         const int st = it % TSTAGES, cb = it % TCONV, kb = it % T_KBUF;
         if (it >= T_KBUF) mbar_wait(kempty + kb, ((it / T_KBUF) - 1) & 1);   // partial read back
         mbar_wait(full + st, (it / TSTAGES) & 1);
@@ -264,8 +295,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
     // ------------------------------------------------------------ converters (warps 2..5)
     const int ct = threadIdx.x - 64;   // 0..127
     int it = 0;
-    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+    const Work<SPLIT> wk(p, ntiles, ktiles);
+    for (int w = 0; w < wk.n; ++w) {
+      for (int kt = wk.kb; kt < wk.ke; ++kt, ++it) {
         const int st = it % TSTAGES, cb = it % TCONV;
         mbar_wait(full + st, (it / TSTAGES) & 1);
         if (it >= TCONV) mbar_wait(cempty + cb, ((it / TCONV) - 1) & 1);
@@ -308,12 +340,13 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
     // ------------------------------------------------------------ accumulate + epilogue (warps 6..9)
     const int q = warp & 3;                 // TMEM lane quarter this warp may access
     int it = 0;
-    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-      const TileCoord c = tile_coord(p, tiles_m, tiles_n, tl);
+    const Work<SPLIT> wk(p, ntiles, ktiles);
+    for (int w = 0; w < wk.n; ++w) {
+      const TileCoord c = tile_coord(p, tiles_m, tiles_n, wk.tl0 + w * wk.step);
       float acc[TBN];
 #pragma unroll
       for (int j = 0; j < TBN; ++j) acc[j] = 0.0f;
-      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+      for (int kt = wk.kb; kt < wk.ke; ++kt, ++it) {
         const int kb = it % T_KBUF;
         mbar_wait(kfull + kb, (it / T_KBUF) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -337,6 +370,35 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
         asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(kempty + kb);   // partial buffer free for the MMAs
+      }
+      if constexpr (SPLIT) {
+        // cluster split-K: park this CTA's partial (row per thread) in the now idle stage
+        // memory, then every CTA sums its 1/S of the rows over the cluster's partials in rank
+        // (= k) order through distributed shared memory and stores them (deterministic)
+        namespace cg = cooperative_groups;
+        cg::cluster_group cl = cg::this_cluster();
+        float* part = reinterpret_cast<float*>(smem);
+        const int row = q * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < TBN; j += 4)
+          *reinterpret_cast<float4*>(part + row * T_PSTRIDE + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+        cl.sync();
+        const int S = p.csplit, r = (int)cl.block_rank(), col = threadIdx.x - 192;   // 0..127
+        const int rows = TBM / S;
+        for (int i = 0; i < rows; ++i) {
+          const int rr = r * rows + i;
+          float v = 0.0f;
+          for (int j = 0; j < S; ++j) v = __fadd_rn(v, cl.map_shared_rank(part, j)[rr * T_PSTRIDE + col]);
+          const int mm = c.m0 + rr, nn = c.n0 + col;
+          if (mm < p.M && nn < p.N) {
+            float o = p.alpha * v;
+            const float* D = p.D[c.s];
+            if (D) o += p.beta * D[c.t * p.sD_t + c.b * p.sD_b + (long long)mm * p.ldd + nn];
+            p.C[c.s][c.t * p.sC_t + c.b * p.sC_b + (long long)mm * p.ldc + nn] = o;
+          }
+        }
+        cl.sync();   // no CTA leaves while its partial may still be read
+        continue;
       }
       const int m = c.m0 + q * 32 + lane;
       if (m >= p.M) continue;
@@ -368,6 +430,11 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
         }
       }
     }
+  }
+  if (SPLIT && warp < 6) {   // the epilogue warps' two cluster barriers, joined by all
+    namespace cg = cooperative_groups;
+    cg::this_cluster().sync();
+    cg::this_cluster().sync();
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -435,7 +502,9 @@ cudaError_t tf32_prepare() {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 32) dev = 0;
   if (done[dev]) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(tf32x3_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM);
+  cudaError_t e = cudaFuncSetAttribute(tf32x3_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(tf32x3_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM);
   if (e == cudaSuccess) done[dev] = true;
   return e;
 }
@@ -484,12 +553,40 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
   else e = make_map(&p.mapT, g.T.hi, g.T, TBK, TBM, true);                      // raw K-major
   if (e != cudaSuccess) return e;
   const long long tiles = (long long)((g.M + TBM - 1) / TBM) * ((g.N + TBN - 1) / TBN) * g.ns * g.nt * g.nb;
-  const int grid = (int)std::min<long long>(tiles, num_sms_tf32());
+  const int nsm = num_sms_tf32();
+  const int grid = (int)std::min<long long>(tiles, nsm);
+  // few tiles (small grids: the stage GEMMs of a 300^2 step have 18): cluster split-K over S CTAs
+  // per tile, the partials reduced through distributed shared memory
+  const int ktiles = (g.kseg + TBK - 1) / TBK * g.nseg;
+  static const bool no_split = getenv("KX_TF32_NOSPLIT") != nullptr;   // diagnostics only
+  int S = 0;
+  if (!no_split && tiles * 2 <= nsm && ktiles >= 4) {
+    S = 8;
+    while (S > 1 && (tiles * S > nsm || ktiles < 2 * S)) S /= 2;
+  }
+  p.csplit = S >= 2 ? S : 0;
   static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only
   if (trace)
-    fprintf(stderr, "kx-tf32 %s M=%d N=%d K=%dx%d z=%dx%dx%d tiles=%lld grid=%d\n",
-            g.kind == TF32_COL ? "col" : "row", g.M, g.N, g.kseg, g.nseg, g.ns, g.nt, g.nb, tiles, grid);
-  tf32x3_gemm_kernel<<<grid, T_THREADS, T_SMEM, stream>>>(p);
+    fprintf(stderr, "kx-tf32 %s M=%d N=%d K=%dx%d z=%dx%dx%d tiles=%lld grid=%d csplit=%d\n",
+            g.kind == TF32_COL ? "col" : "row", g.M, g.N, g.kseg, g.nseg, g.ns, g.nt, g.nb, tiles, grid, p.csplit);
+  if (p.csplit) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(tiles * p.csplit));
+    cfg.blockDim = dim3(T_THREADS);
+    cfg.dynamicSmemBytes = T_SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.csplit;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<true>, p) == cudaSuccess) return cudaSuccess;
+    cudaGetLastError();   // refused (cluster residency): the persistent schedule
+    p.csplit = 0;
+  }
+  tf32x3_gemm_kernel<false><<<grid, T_THREADS, T_SMEM, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -84,13 +84,14 @@ def test_no_half_precision_mma_in_fp64_path(sass):
 def test_fp32_gemm_is_tcgen05_with_tma(sass):
     """fp32 variant: tcgen05 MMA (UTC*MMA) fed by TMA tensor loads (UTMALDG),
     accumulators read back from TMEM (LDTM), TMEM allocated/freed by the kernel."""
-    f = _functions(sass, r"tf32x3_gemm_kernel")
-    assert len(f) == 1
-    f = f[0]
-    assert re.search(r"UTC\w*MMA", f)
-    assert "UTMALDG" in f
-    assert "LDTM" in f
-    assert "DMMA" not in f
+    fs = _functions(sass, r"tf32x3_gemm_kernel")
+    assert len(fs) == 2              # persistent and cluster split-K instantiations
+    for f in fs:
+        assert re.search(r"UTC\w*MMA", f)
+        assert "UTMALDG" in f
+        assert "LDTM" in f
+        assert "DMMA" not in f
+    assert any("UCGABAR" in f for f in fs)   # the split variant's cluster barriers
 
 
 def test_peer_store_gemms_fence_at_system_scope(sass):
