@@ -804,6 +804,17 @@ def run_kx(args, rank, world, sharded):
     return res, cfg, prob
 
 
+def child_env(rank, world, port):
+    """Environment of a child rank with its own rendezvous on 127.0.0.1:port.  Under torchrun the
+    parent's environment says TORCHELASTIC_USE_AGENT_STORE=True (the agent hosts the TCPStore),
+    which would make every child a store CLIENT of a server nobody starts on the new port: the
+    TORCHELASTIC_* variables are dropped so that the child rank 0 hosts it."""
+    env = {k: v for k, v in os.environ.items() if not k.startswith("TORCHELASTIC_")}
+    env.update(RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port),
+               LOCAL_RANK=os.environ.get("LOCAL_RANK", str(rank)), NCCL_DEBUG="INFO")
+    return env
+
+
 def sharded_subrun(args, rank, world, timeout_s=480):
     """N > 1 replicas runs also measure the north_star's multi-GPU workload: C4 (512^3)
     slab-sharded over the same GPUs (direct peer stores + NCCL barriers), in child processes
@@ -822,9 +833,7 @@ def sharded_subrun(args, rank, world, timeout_s=480):
     dist.broadcast_object_list(port, src=0)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
-    env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
-               MASTER_PORT=str(port[0]), LOCAL_RANK=os.environ.get("LOCAL_RANK", str(rank)),
-               NCCL_DEBUG="INFO")
+    env = child_env(rank, world, port[0])
     steps = 10
     cmd = [sys.executable, os.path.abspath(__file__), "--gpus", str(world), "--config", "C4",
            "--mode", "sharded", "--steps", str(steps), "--warmup", "3", "--no-extras"]
