@@ -490,6 +490,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // Programmatic dependent launch: this CTA may have started while the previous kernel of the
+  // stream was still draining (its SM freed early); wait for that grid's completion and memory
+  // flush before the first global access, and let the next kernel's CTAs be scheduled as SMs
+  // free up.  Both are no-ops for a launch without the attribute.
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
   // ---- producer
   WorkIter pit;
@@ -907,6 +913,17 @@ double plan_cfg(const GemmArgs& g, int nz, double eff, Sched& sc) {
   return best;
 }
 
+// Programmatic dependent launch of the GEMMs: opt-in (KX_PDL=1).  Measured slower in the step
+// graphs (C2 2.644 vs 2.623, C3 1.720 vs 1.712 ms/step): the next GEMM's early CTAs gain no
+// prologue work worth the SMs they hold while the previous grid's stream-K reducers finish.
+bool pdl_on() {
+  static const bool on = [] {
+    const char* e = getenv("KX_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 const TmaMaps& no_maps() {
   static const TmaMaps m = {};
   return m;
@@ -934,13 +951,15 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t strea
     cfg.blockDim = dim3(C_::NT);
     cfg.dynamicSmemBytes = C_::SMEM;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = sc.csplit;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc, tm);
     if (ce == cudaSuccess) return ce;
     // the cluster launch was refused (e.g. SMs taken by concurrent work): plain data-parallel
@@ -959,11 +978,13 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t strea
     cfg.blockDim = dim3(C_::NT);
     cfg.dynamicSmemBytes = C_::SMEM;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     const cudaError_t ce = cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc, tm);
     if (ce != cudaErrorCooperativeLaunchTooLarge) return ce;
     // not all CTAs can be co-resident right now: the data-parallel schedule needs no waits
@@ -973,8 +994,19 @@ cudaError_t launch_cfg(const GemmArgs& g, int nz, double eff, cudaStream_t strea
     sc.sk_units = 0;
     sc.G_sk = 0;
   }
-  gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER><<<dim3(sc.G), C_::NT, C_::SMEM, stream>>>(g, sc, tm);
-  return cudaGetLastError();
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(sc.G);
+    cfg.blockDim = dim3(C_::NT);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<BM, BN, BK, WM, WN, AROW, VEC, STAGES, PEER>, g, sc, tm);
+  }
 }
 
 // ---------------------------------------------------------------- TMA tensor maps (VEC == 3)
