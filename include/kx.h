@@ -169,13 +169,14 @@ kx_status kx_set_fused_small(kx_ctx *ctx, int on);
  * i_d in [rank n_d/P, (rank+1) n_d/P) in vec order (N/P doubles).  kx_step then performs the
  * sharded step with NCCL all-to-all exchanges (ncclSend/ncclRecv groups, fp64) enqueued on the
  * context stream.
- * The operators kx_tucker, kx_mode_product and kx_phi_apply also work on NCCL ranks, on the
+ * The operators kx_tucker, kx_mode_product, kx_phi_apply and kx_kronsum (dense A_mu: the mode-d
+ * term through the exchange) also work on NCCL ranks, on the
  * rank's layout-A slab X, Y (N/P doubles each; the matrices / bank are global): modes 1..d-1
  * are local; an operator that contracts mode d runs [A] pack by i_1 block -> all-to-all ->
  * [B] modes d..2 on full fibres -> all-to-all -> [A] mode 1 as one concatenated-K GEMM over the
  * source ranks' chunks (alpha, beta in its epilogue), so it matches one GPU up to rounding
  * (BASELINE.json configs[4] at 2-8 GPUs).  Collective: every rank calls it with the
- * same arguments apart from X, Y.  kx_tucker_batched, kx_kronsum and kx_integrate_host return
+ * same arguments apart from X, Y.  kx_tucker_batched and kx_integrate_host return
  * KX_ERR_UNSUPPORTED on distributed contexts. */
 /* 128-byte ncclUniqueId (NCCL from the process, dlopen'ed); create on rank 0, broadcast. */
 kx_status kx_nccl_unique_id(void *out128);
@@ -197,6 +198,8 @@ kx_status kx_tucker_group(kx_ctx *const *ctxs, int nranks, const double *const *
                           const double *const *L, double alpha, double beta);
 kx_status kx_mode_product_group(kx_ctx *const *ctxs, int nranks, const double *const *X,
                                 double *const *Y, int mu, const double *L, double alpha, double beta);
+kx_status kx_kronsum_group(kx_ctx *const *ctxs, int nranks, int comp, const double *const *X,
+                           double *const *Y, double beta);
 kx_status kx_phi_apply_group(kx_ctx *const *ctxs, int nranks, int comp, int ell, int stage,
                              const double *const *X, double *const *Y, double alpha, double beta);
 /* Direct peer stores: the kernel producing each exchanged tensor (stencil F,

@@ -415,7 +415,7 @@ kx_status kx_tucker_batched(kx_ctx* c, int nbatch, const double* X, double* Y, c
 kx_status kx_kronsum(kx_ctx* c, int comp, const double* X, double* Y, double beta) {
   DevGuard dg_(c);
   KX_TRY(need_grid(c));
-  if (c->dist) return fail(c, KX_ERR_UNSUPPORTED, "single-GPU operator on a distributed context");
+  if (c->dist == 2) return fail(c, KX_ERR_INVALID, "loopback group members use kx_kronsum_group");
   if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
   for (int mu = 1; mu <= c->d; ++mu)
     if (!c->A_dev[comp][mu - 1])
@@ -424,6 +424,15 @@ kx_status kx_kronsum(kx_ctx* c, int comp, const double* X, double* Y, double bet
   KX_TRY(check_ptr(c, Y, "Y"));
   if (X == Y) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
   c->cur = c->stream;
+  if (c->dist == 1) {   // slab-sharded: modes 1..d-1 local, mode d through the exchange
+    DistOp op;
+    op.kind = 3;
+    op.X = X;
+    op.Y = Y;
+    op.beta = beta;
+    op.comp = comp;
+    return dist_op_nccl(c, op);
+  }
   const double* Xs[1] = {X};
   double* Ys[1] = {Y};
   const double* Ds[1] = {Y};
@@ -926,6 +935,30 @@ kx_status kx_mode_product_group(kx_ctx* const* ctxs, int nranks, const double* c
     ops[r].beta = beta;
   }
   if (mu < ctxs[0]->d) return KX_OK;
+  return group_op(ctxs, nranks, ops);
+}
+
+kx_status kx_kronsum_group(kx_ctx* const* ctxs, int nranks, int comp, const double* const* X, double* const* Y,
+                           double beta) {
+  DevGuard dg_(ctxs && nranks > 0 ? ctxs[0] : nullptr);
+  KX_TRY(group_members(ctxs, nranks));
+  if (!X || !Y) return fail(ctxs[0], KX_ERR_INVALID, "X or Y is NULL");
+  std::vector<DistOp> ops(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    kx_ctx* c = ctxs[r];
+    if (comp < 0 || comp >= c->ncomp) return fail(c, KX_ERR_INVALID, "comp out of range");
+    for (int mu = 1; mu <= c->d; ++mu)
+      if (!c->A_dev[comp][mu - 1])
+        return fail(c, KX_ERR_INVALID, "direction matrix mu=" + std::to_string(mu) + " not set");
+    KX_TRY(check_ptr(c, X[r], "X[r]"));
+    KX_TRY(check_ptr(c, Y[r], "Y[r]"));
+    if (X[r] == Y[r]) return fail(c, KX_ERR_INVALID, "X and Y must be distinct");
+    ops[r].kind = 3;
+    ops[r].X = X[r];
+    ops[r].Y = Y[r];
+    ops[r].beta = beta;
+    ops[r].comp = comp;
+  }
   return group_op(ctxs, nranks, ops);
 }
 

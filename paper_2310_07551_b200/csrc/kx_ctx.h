@@ -350,7 +350,8 @@ kx_status nccl_exchange(kx_ctx* c, const Exchange& x, cudaStream_t st);
 kx_status dist_step_nccl(kx_ctx* c, double* const* U);
 // ---- kx_dist_ops.cpp: distributed operators (Tucker, mode product, split phi-action)
 struct DistOp {
-  int kind = 0;                      // 0 Tucker, 1 split phi-action, 2 mode product along mu = d
+  int kind = 0;                      // 0 Tucker, 1 split phi-action, 2 mode product along mu = d,
+                                     // 3 Kronecker-sum action (dense A_mu of component comp)
   const double* X = nullptr;         // layout-A slab (Nloc doubles)
   double* Y = nullptr;
   const double* L[KX_MAXD] = {};     // Tucker matrices / the mode-d matrix in L[d-1]

@@ -1,6 +1,7 @@
-// Distributed operators: the Tucker operator, the mu-mode product and
-// the split phi-action (eq:split2d / eq:splitnd3 via eq:krontomu) on a
-// slab-sharded context (BASELINE.json configs[4], the Tucker sweep at 2-8 GPUs).
+// Distributed operators: the Tucker operator, the mu-mode product, the
+// split phi-action (eq:split2d / eq:splitnd3 via eq:krontomu) and the
+// Kronecker-sum action (eq:kronsumv: the mode-d term through the exchange, the other
+// terms local, summed into Y by the unpack) on a slab-sharded context (BASELINE.json configs[4], the Tucker sweep at 2-8 GPUs).
 //
 // The user's tensors are layout-A slabs (i_d sharded, n_d / P planes per rank).  Modes 1..d-1
 // are local in layout A; mode d needs whole i_d fibres, which layout B (i_1 sharded) holds.  An
@@ -91,6 +92,14 @@ kx_status dist_op_phase(kx_ctx* c, const DistOp& op, int ph, Exchange& x) {
       for (int t = 0; t < ps.nterms; ++t) x.add(ws[0] + (long long)t * c->Nloc, c->RA[0] + (long long)t * c->Nloc);
       return KX_OK;
     }
+    if (op.kind == 3) {   // the mode-d term of the Kronecker sum
+      const double* Xs[1] = {c->dop[1]};
+      double* Ys[1] = {c->dop[2]};
+      const double* Ls[1] = {c->A_dev[op.comp][d - 1]};
+      KX_TRY(mode_product_multi(c, 1, Xs, Ys, d, Ls, 1.0, 0.0, nullptr));
+      x.add(c->dop[2], c->dop[4]);
+      return KX_OK;
+    }
     const double* src = c->dop[1];
     double* bufs[2] = {c->dop[2], c->dop[3]};
     int w = 0;
@@ -109,6 +118,22 @@ kx_status dist_op_phase(kx_ctx* c, const DistOp& op, int ph, Exchange& x) {
   }
   // [A] ph == 2
   set_layout(c, false);
+  if (op.kind == 3) {   // Y = beta Y + sum_{mu < d} X x_mu A_mu (local), then + the mode-d term
+    double beta = op.beta;
+    for (int mu = 1; mu < d; ++mu) {
+      const double* Xs[1] = {op.X};
+      double* Ys[1] = {op.Y};
+      const double* Ls[1] = {c->A_dev[op.comp][mu - 1]};
+      const double* Ds[1] = {op.Y};
+      KX_TRY(mode_product_multi(c, 1, Xs, Ys, mu, Ls, 1.0, beta, Ds));
+      beta = 1.0;
+    }
+    KX_TRY(run_other(c, [&] {
+      return kx::launch_copy2d_axpby(op.Y, n1, n1l, c->dop[4], n1l, chunk, rows, n1l, P, 1.0, beta, c->cur);
+    }, 24.0 * (double)c->Nloc));
+    c->cnt.kronsum_actions += 1;
+    return KX_OK;
+  }
   if (op.kind == 2) {   // unpack: Y[row, q n1l + j] = R_q[row, j] + beta Y
     KX_TRY(run_other(c, [&] {
       return kx::launch_copy2d_axpby(op.Y, n1, n1l, c->dop[4], n1l, chunk, rows, n1l, P, 1.0, op.beta, c->cur);

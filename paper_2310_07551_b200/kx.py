@@ -72,6 +72,7 @@ _SIGS = {
     "kx_tucker_group": (_i, [C.POINTER(_vp), _i, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp), _d, _d]),
     "kx_mode_product_group": (_i, [C.POINTER(_vp), _i, C.POINTER(_vp), C.POINTER(_vp), _i, _vp, _d, _d]),
     "kx_phi_apply_group": (_i, [C.POINTER(_vp), _i, _i, _i, _i, C.POINTER(_vp), C.POINTER(_vp), _d, _d]),
+    "kx_kronsum_group": (_i, [C.POINTER(_vp), _i, _i, C.POINTER(_vp), C.POINTER(_vp), _d]),
     "kx_group_set_p2p": (_i, [C.POINTER(_vp), _i, _i]),
     "kx_dist_ipc_export": (_i, [_vp, _vp, C.c_size_t, C.POINTER(C.c_size_t)]),
     "kx_dist_ipc_import": (_i, [_vp, _vp, C.c_size_t]),
@@ -446,6 +447,9 @@ class Group:
         nm = c0.n[mu - 1] if 1 <= mu <= c0.d else None
         self._chk(kx_mode_product_group(self._arr, self.nranks, self._slabs(Xs), self._slabs(Ys), mu,
                                         _ptr(L, nm * nm if nm else None, c0.device), alpha, beta))
+
+    def kronsum(self, comp: int, Xs: list, Ys: list, beta=0.0):
+        self._chk(kx_kronsum_group(self._arr, self.nranks, comp, self._slabs(Xs), self._slabs(Ys), beta))
 
     def phi_apply(self, comp: int, ell: int, stage: int, Xs: list, Ys: list, alpha=1.0, beta=0.0):
         self._chk(kx_phi_apply_group(self._arr, self.nranks, comp, ell, stage, self._slabs(Xs),
