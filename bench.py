@@ -637,6 +637,51 @@ def sharded_closed_form_check(kx, torch, stream, cfg, n, rank, world, dist):
         ctx.close()
 
 
+def sharded_tucker(kx, torch, stream, rank, world, dist, sizes=(512, 1024), reps=3):
+    """C5 at P GPUs (BASELINE.json configs[4]): one d = 3 Tucker operator on an n^3 tensor slab-
+    sharded over the ranks (kx_tucker on NCCL ranks: pack, all-to-all, modes 3..2 on full fibres,
+    all-to-all, concatenated-K mode 1), dense flops 2 N d n over the max-over-ranks device time."""
+    out = {}
+    peak = load_peak()[0] if rank == 0 else None
+    for n in sizes:
+        N = n ** 3
+        uid = [kx.nccl_unique_id() if rank == 0 else None]
+        if dist is not None:
+            dist.broadcast_object_list(uid, src=0)
+        ctx = kx.Context(torch.cuda.current_device(), stream, dist=(uid[0], rank, world))
+        try:
+            ctx.set_grid([n, n, n], 1)
+            X = torch.rand(N // world, dtype=torch.float64, device="cuda")
+            Y = torch.empty_like(X)
+            Ls = [torch.rand(n * n, dtype=torch.float64, device="cuda") / n for _ in range(3)]
+            ctx.tucker(X, Y, Ls)
+            ctx.sync()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if dist is not None:
+                dist.barrier()
+            with torch.cuda.stream(stream):
+                e0.record()
+                for _ in range(reps):
+                    ctx.tucker(X, Y, Ls)
+                e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            if dist is not None:
+                t = torch.tensor([ms], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            tf = 2.0 * N * 3 * n / ms / 1e9
+            out[f"d3_n{n}"] = {"ms": round(ms, 3), "tflops": round(tf, 2),
+                               "frac_of_P_dmma": round(tf / (world * peak), 3) if peak else None}
+            del X, Y, Ls
+        except Exception as e:
+            out[f"d3_n{n}"] = {"error": str(e)[:200]}
+        finally:
+            ctx.close()
+            torch.cuda.empty_cache()
+    return out
+
+
 def run_kx(args, rank, world, sharded):
     import torch
     import inputs
@@ -789,6 +834,7 @@ def run_kx(args, rank, world, sharded):
         torch.cuda.empty_cache()
         res["check"] = sharded_closed_form_check(kx, torch, stream, cfg, prob.n, rank, world,
                                                  dist if world > 1 else None)
+        res["tucker_sharded"] = sharded_tucker(kx, torch, stream, rank, world, dist if world > 1 else None)
     if not args.no_extras and rank == 0 and not sharded:
         del U, flush
         torch.cuda.empty_cache()
@@ -849,6 +895,7 @@ def sharded_subrun(args, rank, world, timeout_s=480):
                        "n_gpus": d["n_gpus"], "scaling": d["scaling"],
                        "workload": d["config"]["workload"], "parallelism": d["config"]["parallelism"],
                        "exchange": d.get("exchange"), "check": d.get("check"),
+                       "tucker_sharded": d.get("tucker_sharded"),
                        "roofline_frac": d["roofline"]["frac"], "clocks": d.get("clocks"),
                        "finite": d.get("finite")}
             else:
@@ -967,6 +1014,8 @@ def main():
         line["exchange"] = res.get("exchange")
         if res.get("check"):
             line["check"] = res["check"]
+        if res.get("tucker_sharded"):
+            line["tucker_sharded"] = res["tucker_sharded"]
     if "e2e_ms" in res:
         line["e2e"] = {"value": (1 if sharded else world) * 1e3 / res["e2e_ms"], "unit": "steps/s",
                        "h2d_bytes_per_step": res["e2e_bytes"], "d2h_bytes_per_step": res["e2e_bytes"]}
