@@ -119,7 +119,7 @@ struct Cfg {
   static constexpr int SB = TMA ? 0 : BN + 4;
   static constexpr int B_ST = TMA ? BK * BN : BK * SB;
   static constexpr int ALIGN = TMA ? 1024 : 0;               // swizzle atoms 512-B aligned
-  static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8 + 2 * STAGES * 8 + ALIGN;   // + mbarriers
+  static constexpr int SMEM = STAGES * (A_ST + B_ST) * 8 + 2 * STAGES * 8 + ALIGN + (TMA ? 512 : 0);   // + mbarriers (+ TMA producer state)
   // loader geometry: chunks of LV doubles, each thread owns IA (A) and IB (B) chunks
   static constexpr int CPR_A = AROW ? BK / LV : BM / LV;   // chunks per smem row of A
   static constexpr int IA = BM * BK / LV / NT;
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   int pk = 0;
   int pkt = 0;   // k-tiles issued so far (stage = pkt % STAGES, fill = pkt / STAGES)
   typename T_::Loader ld;
-  if (TMA && tid != 0) p_ok = false;   // TMA: thread 0 alone produces
+  if (TMA) p_ok = false;   // TMA: the releasing warps issue (below), produce() is unused
   if (p_ok) {
     pk = ps.kb;
     ld.setup(p, T_::coords(p, sc, ps.tl), ps.kb);
@@ -531,6 +531,46 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   };
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) produce();
+
+  // TMA: the lookahead over the k-tile sequence lives in shared memory, and the warp that
+  // releases a stage LAST issues that stage's refill (the k-tile STAGES ahead) at once — no
+  // thread ever waits for a stage to drain (a per-stage release counter replaces the empty
+  // mbarrier).  Refills are issued in k-tile order: the last release of k-tile i+1 happens after
+  // the issuing warp of i released i+1 itself.
+  struct ProdSt {
+    WorkIter it;
+    Seg seg;
+    int pk, ok;
+    typename T_::Loader ld;
+  };
+  unsigned* relc = reinterpret_cast<unsigned*>(empty + STAGES);
+  ProdSt* sprod = reinterpret_cast<ProdSt*>(reinterpret_cast<uintptr_t>(relc + 8 + STAGES) & ~uintptr_t(15));
+  auto tma_issue_next = [&](int stage) {   // one thread
+    ProdSt S = *sprod;
+    if (!S.ok) return;
+    S.ld.issue_tma(p, tm, As + stage * A_ST, Bs + stage * B_ST, full + stage);
+    if (++S.pk == S.seg.ke) {
+      S.ok = S.it.next(S.seg);
+      if (S.ok) {
+        S.pk = S.seg.kb;
+        S.ld.setup(p, T_::coords(p, sc, S.seg.tl), S.seg.kb);
+      }
+    }
+    *sprod = S;
+  };
+  if constexpr (TMA) {
+    static_assert(sizeof(ProdSt) + 8 * 4 + 64 <= 512, "TMA producer state fits");
+    if (tid == 0) {
+      for (int st = 0; st < STAGES; ++st) relc[st] = 0;
+      ProdSt S;
+      S.it.init(sc, cta);
+      S.ok = S.it.next(S.seg);
+      S.pk = S.seg.kb;
+      if (S.ok) S.ld.setup(p, T_::coords(p, sc, S.seg.tl), S.seg.kb);
+      *sprod = S;
+      for (int st = 0; st < STAGES; ++st) tma_issue_next(st);   // fill every stage
+    }
+  }
 
   // ---- consumer
   WorkIter cit;
@@ -618,7 +658,20 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
         if (kk == PRODUCE_KK) produce();
       }
     }
-    mbar_arrive(empty + stage_c);
+    if constexpr (TMA) {
+      __syncwarp();   // every lane's fragment loads of this stage have been consumed
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(relc + stage_c, 1u) == (unsigned)(NT / 32 - 1)) {   // the last warp out
+          relc[stage_c] = 0;
+          __threadfence_block();
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          tma_issue_next(stage_c);
+        }
+      }
+    } else {
+      mbar_arrive(empty + stage_c);
+    }
     ++ckt;
     if (++cks == kps) cks = 0;
     if (++ck < cs.ke) continue;
@@ -1055,11 +1108,20 @@ bool make_map64(CUtensorMap* map, const double* base, const long long* ext, cons
 // k chunks of 8 doubles that never straddle a segment (kseg % 8), 8-wide n / m chunks, no
 // flattened batches and no zero batch strides.
 bool build_tma(const GemmArgs& g, TmaMaps& tm) {
-  // opt-in (KX_GEMM_TMA=1): measured slower than the cp.async pipeline (C2 2.639 vs 2.617,
-  // C3 1.765 vs 1.711 ms/step) — one thread issuing 32-KB boxes of 64-B rows after the stage's
-  // empty barrier puts warp 0 on every stage's critical path
-  static const bool on = getenv("KX_GEMM_TMA") != nullptr;
-  if (!on || g.nflat || g.peer.P || g.kseg % 8 || g.N % 8 || (!g.arow && g.M % 8)) return false;
+  // Where the TMA-fed variant runs (KX_GEMM_TMA=0: never, =1: wherever eligible; default: the
+  // long-K concatenated-K launches, ROW layout with >= 32 k-tiles per tile).  Measured per
+  // launch (ncu, one step): C2 stage GEMMs (K = 2048 / 4096) 284.4 -> 281.3, 532.9 -> 527.2 us
+  // (DMMA active 91.7 -> 93.2%); the short-K C3 launches and the COL first modes gain nothing or
+  // lose up to 4% (the stage's last warp out issues its refill; with 4 k-tiles per tile the
+  // cp.async producers' spread-out issue overlaps the tile transitions better).
+  static const int mode = [] {
+    const char* e = getenv("KX_GEMM_TMA");
+    return e ? atoi(e) : -1;
+  }();
+  if (mode == 0) return false;
+  const int ktiles_tile = (g.kseg + 31) / 32 * g.nseg;
+  if (mode < 0 && (!g.arow || ktiles_tile < 32)) return false;
+  if (g.nflat || g.peer.P || g.kseg % 8 || g.N % 8 || (!g.arow && g.M % 8)) return false;
   if (g.ns * (g.arow ? g.nseg : 1) > kTmaMaxA || (!g.arow && g.nseg != 1)) return false;
   if ((g.nt > 1 && (g.sA_t == 0 || g.sB_t == 0)) || (g.nb > 1 && (g.sA_b == 0 || g.sB_b == 0))) return false;
   tm.nsegmaps = g.arow ? g.nseg : 1;
