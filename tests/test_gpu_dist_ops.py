@@ -209,3 +209,37 @@ def test_kronsum_group(kx, case):
     ref = vec(kronsum_apply(unvec(x, n), As)) + 0.5 * y0
     assert relerr(assemble(Ys, n, P), ref) <= 1e-12
     g.close()
+
+
+@pytest.mark.parametrize("scheme", ["etd3rkds", "exprk3ds_cplx"])
+def test_nccl_one_rank_phi_apply_and_kronsum(kx, scheme):
+    """kx_phi_apply and kx_kronsum through the NCCL path of a one-rank distributed context equal
+    the single-GPU calls to rounding (every (ell, stage) of the bank, both components)."""
+    prob = inputs.make_problem("fhn", 3, [24, 20, 16], seed=4)
+    tau = 0.015
+    uid = kx.nccl_unique_id()
+    ctxs = [kx.Context(0, dist=(uid, 0, 1)), kx.Context(0)]
+    for c in ctxs:
+        c.set_grid(prob.n, 2)
+        for s in range(2):
+            for mu in range(3):
+                c.set_direction_matrix(s, mu + 1, prob.A[s][mu])
+        c.set_model(prob.model, prob.params)
+        c.set_tau(tau, scheme)
+    x = dev(inputs.uniform_sym(91, 0, prob.N))
+    y0 = inputs.uniform_sym(92, 0, prob.N)
+    for comp in range(2):
+        for ell, stage in [(1, 0), (1, 1), (1, 2), (2, 1), (2, 2)]:
+            Ys = [dev(y0), dev(y0)]
+            for c, Y in zip(ctxs, Ys):
+                c.phi_apply(comp, ell, stage, x, Y, 0.5, 1.0)
+                c.sync()
+            assert relerr(Ys[0].cpu().numpy(), Ys[1].cpu().numpy()) <= 1e-13, (comp, ell, stage)
+        Ys = [dev(y0), dev(y0)]
+        for c, Y in zip(ctxs, Ys):
+            c.set_kronsum_mode(True)     # dense A_mu on both (the sharded kronsum is dense)
+            c.kronsum(comp, x, Y, 0.25)
+            c.sync()
+        assert relerr(Ys[0].cpu().numpy(), Ys[1].cpu().numpy()) <= 1e-13
+    for c in ctxs:
+        c.close()
