@@ -72,18 +72,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-// VEC == 3: the operand tiles arrive by TMA (cp.async.bulk.tensor, issued by one thread) into an
-// unpadded 64-B-swizzled layout: a tile is stored as slabs of 8 doubles (one 64-B row) per
-// (chunk, row), [chunk][row][8], and 16-B unit u of byte offset o within a 512-B span lands at
-// u ^ ((o >> 7) & 3) (CU_TENSOR_MAP_SWIZZLE_64B).  Every m8n8k4 fragment load of both layouts is
-// then conflict-free (2 wavefronts per 256 B), as with the padded cp.async layout.
+// VEC == 3: the operand tiles arrive by TMA (cp.async.bulk.tensor) in FRAGMENT ORDER: the 4-D
+// boxes are chosen so that the 32 doubles one m8n8k4 fragment load of a warp reads are one
+// contiguous 256-B block of shared memory whose two 128-B halves are lanes 0-15 and 16-31 (a
+// 64-bit shared load is served per half-warp): 2 wavefronts, no bank conflicts, no swizzle:
+//   B and COL A (k rows, n / m contiguous): box {4 n, 4 k, n/4, k/4} -> [k/4][n/4][k%4][n%4];
+//   ROW A (m rows, k contiguous): box {4 k, 8 m, k/4, m/8} -> [m/8][k/4][m%8][k%4].
+// (Tried first: a 64-B-swizzled [chunk][row][8] layout — rows k and k+2 share banks — and
+// [k/4][n/8][k%4][n%8] — lanes 0-15 then span all 256 B: 2-way conflicts either way.)
 constexpr int kTmaMaxA = 16;   // A maps: species x concatenated-K segments
 struct TmaMaps {
   CUtensorMap A[kTmaMaxA];
   CUtensorMap B[MAXS];
   int nsegmaps = 1;            // A map of (species s, segment j) = A[s * nsegmaps + j]
 };
-__device__ __forceinline__ unsigned swz64(unsigned o) { return o ^ (((o >> 7) & 3u) << 4); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -303,9 +305,9 @@ struct GemmTile {
                                               uint64_t* bar) {
       mbar_expect_tx(bar, (BM * BK + BK * BN) * 8);
       const CUtensorMap* mA = &tm.A[tc.s * tm.nsegmaps + (AROW ? lseg : 0)];
-      if constexpr (AROW) tma_load5(as, mA, 0, tc.m0, lk0 / 8, tc.t, tc.b, bar);   // [kc][m][8]
-      else tma_load5(as, mA, 0, lk0, tc.m0 / 8, tc.t, tc.b, bar);                   // [mc][k][8]
-      tma_load5(bs, &tm.B[tc.s], 0, lseg * p.kseg + lk0, tc.n0 / 8, tc.t, tc.b, bar);   // [nc][k][8]
+      if constexpr (AROW) tma_load5(as, mA, 0, 0, lk0 / 4, tc.m0 / 8, tc.t, bar);   // [m/8][k/4][8][4]
+      else tma_load5(as, mA, 0, 0, tc.m0 / 4, lk0 / 4, tc.t, bar);                 // [k/4][m/4][4][4]
+      tma_load5(bs, &tm.B[tc.s], 0, 0, tc.n0 / 4, (lseg * p.kseg + lk0) / 4, tc.t, bar);   // [k/4][n/4][4][4]
       lk0 += BK;
       if (lk0 >= p.kseg) {
         lk0 = 0;
@@ -597,35 +599,27 @@ __global__ void __launch_bounds__(Cfg<BM, BN, BK, WM, WN, AROW, VEC, STAGES>::NT
   const int kps = (p.kseg + BK - 1) / BK;
   const int ktail = p.kseg - (kps - 1) * BK;   // valid k of a segment's last k-tile
   int cks = ck % kps;                          // k-tile position inside its segment
-  // TMA layout: per-thread byte offsets of this thread's fragment element for kk % 8 == 0 / 4
-  // (AROW A: row m = wm0 + g + 8i in slab kk / 8; COL A and B: row k = kk + t4 of slab
-  // (wm0 or wn0) / 8 + i); the XOR of swz64 folded in
-  int tma_a[2] = {0, 0}, tma_b[2] = {0, 0};
+  // TMA (fragment-ordered) layout: this thread's byte offset inside the 256-B block of a fragment
+  int tma_a = 0, tma_b = 0;
   if constexpr (TMA) {
-    for (int par = 0; par < 2; ++par) {
-      const int row_k = par * 4 + t4;          // k within the 8-row group (kk & 7 = 4 par)
-      const unsigned gsw = swz64((unsigned)(row_k * 64 + g * 8));   // rows of 64 B, 8 doubles
-      if constexpr (AROW) tma_a[par] = (int)swz64((unsigned)((wm0 + g) * 64 + row_k * 8));
-      else tma_a[par] = (wm0 >> 3) * (BK * 64) + (int)gsw;
-      tma_b[par] = (wn0 >> 3) * (BK * 64) + (int)gsw;
-    }
+    if constexpr (AROW) tma_a = (wm0 >> 3) * (BK / 4) * 256 + g * 32 + t4 * 8;
+    else tma_a = ((wm0 >> 2) * 16 + (g >> 2) * 16 + t4 * 4 + (g & 3)) * 8;
+    tma_b = ((wn0 >> 2) * 16 + (g >> 2) * 16 + t4 * 4 + (g & 3)) * 8;
   }
   auto kstep = [&](const double* as, const double* bs, int kk) {
     double af[FM], bf[FN];
     if constexpr (TMA) {
-      // [chunk][row][8] slabs, 64-B swizzle (see swz64): per-thread offsets for the two k-step
-      // parities (kk & 4) are precomputed (tma_off), the rest are compile-time immediates
+      // one contiguous 256-B block per fragment; block index from (k/4, chunk) as immediates
       const char* a8 = reinterpret_cast<const char*>(as);
       const char* b8 = reinterpret_cast<const char*>(bs);
-      const int par = (kk >> 2) & 1;
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
-        if constexpr (AROW) af[i] = *reinterpret_cast<const double*>(a8 + (kk >> 3) * (BM * 64) + i * 512 + tma_a[par]);
-        else af[i] = *reinterpret_cast<const double*>(a8 + i * (BK * 64) + (kk & ~7) * 64 + tma_a[par]);
+        if constexpr (AROW) af[i] = *reinterpret_cast<const double*>(a8 + (i * (BK / 4) + (kk >> 2)) * 256 + tma_a);
+        else af[i] = *reinterpret_cast<const double*>(a8 + (kk >> 2) * (BM * 32) + i * 256 + tma_a);
       }
 #pragma unroll
       for (int j = 0; j < FN; ++j)
-        bf[j] = *reinterpret_cast<const double*>(b8 + j * (BK * 64) + (kk & ~7) * 64 + tma_b[par]);
+        bf[j] = *reinterpret_cast<const double*>(b8 + (kk >> 2) * (BN * 32) + j * 256 + tma_b);
     } else {
 #pragma unroll
       for (int i = 0; i < FM; ++i) {
@@ -1080,13 +1074,15 @@ EncodeTiledFn tma_encoder() {
   return fn;
 }
 
-// 5-D fp64 view (element extents / strides, stride[0] = 1) with box {8, b1, b2, 1, 1} and the
-// 64-B swizzle; extent-1 dims get a packed stride; false if TMA cannot express the view.
-bool make_map64(CUtensorMap* map, const double* base, const long long* ext, const long long* str, int b1, int b2) {
+// 5-D fp64 view (element extents / strides, stride[0] = 1) with the given box, no swizzle;
+// extent-1 dims get a packed stride; false if TMA cannot express the view.
+bool make_map64(CUtensorMap* map, const double* base, const long long* ext, const long long* str,
+                const int* boxd) {
   EncodeTiledFn enc = tma_encoder();
   if (!enc || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
   cuuint64_t dims[5], strides[4];
-  cuuint32_t box[5] = {8, (cuuint32_t)b1, (cuuint32_t)b2, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) box[i] = (cuuint32_t)boxd[i];
   long long prev = 1;
   for (int i = 0; i < 5; ++i) {
     if (ext[i] < 1 || ext[i] > (1LL << 32)) return false;
@@ -1100,7 +1096,7 @@ bool make_map64(CUtensorMap* map, const double* base, const long long* ext, cons
     prev = st;
   }
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1109,35 +1105,41 @@ bool make_map64(CUtensorMap* map, const double* base, const long long* ext, cons
 // flattened batches and no zero batch strides.
 bool build_tma(const GemmArgs& g, TmaMaps& tm) {
   // Where the TMA-fed variant runs (KX_GEMM_TMA=0: never, =1: wherever eligible; default: the
-  // long-K concatenated-K launches, ROW layout with >= 32 k-tiles per tile).  Measured per
-  // launch (ncu, one step): C2 stage GEMMs (K = 2048 / 4096) 284.4 -> 281.3, 532.9 -> 527.2 us
-  // (DMMA active 91.7 -> 93.2%); the short-K C3 launches and the COL first modes gain nothing or
-  // lose up to 4% (the stage's last warp out issues its refill; with 4 k-tiles per tile the
-  // cp.async producers' spread-out issue overlaps the tile transitions better).
+  // long-K launches, >= 32 k-tiles per tile).  Measured per launch (ncu, one step, conflict-free
+  // fragment-ordered boxes): C2 DMMA active 92.4 -> 93.4% (first mode, K = 1024), 88.7 -> 89.2%
+  // (D2 / D3 first modes), 91.7 -> 93.5% (stage GEMMs, K = 2048 / 4096); C2 2.618 -> 2.579
+  // ms/step.  The short-K (K = 128: 4 k-tiles per tile) C3 launches lose up to 5% with it.
   static const int mode = [] {
     const char* e = getenv("KX_GEMM_TMA");
     return e ? atoi(e) : -1;
   }();
   if (mode == 0) return false;
   const int ktiles_tile = (g.kseg + 31) / 32 * g.nseg;
-  if (mode < 0 && (!g.arow || ktiles_tile < 32)) return false;
+  if (mode < 0 && ktiles_tile < 32) return false;
   if (g.nflat || g.peer.P || g.kseg % 8 || g.N % 8 || (!g.arow && g.M % 8)) return false;
   if (g.ns * (g.arow ? g.nseg : 1) > kTmaMaxA || (!g.arow && g.nseg != 1)) return false;
-  if ((g.nt > 1 && (g.sA_t == 0 || g.sB_t == 0)) || (g.nb > 1 && (g.sA_b == 0 || g.sB_b == 0))) return false;
+  // the fragment-ordered boxes use 4 of the 5 dims; the fifth carries the t batch (nb == 1)
+  if (g.nb > 1 || (g.nt > 1 && (g.sA_t == 0 || g.sB_t == 0)) || g.M % 8) return false;
   tm.nsegmaps = g.arow ? g.nseg : 1;
   for (int s = 0; s < g.ns; ++s) {
     for (int j = 0; j < tm.nsegmaps; ++j) {
-      const long long ext_r[5] = {8, g.M, g.kseg / 8, g.nt, g.nb};
-      const long long ext_c[5] = {8, g.kseg, g.M / 8, g.nt, g.nb};
-      const long long str[5] = {1, g.lda, 8, g.sA_t, g.sA_b};
+      // ROW A (m rows, k contiguous): (4 k, 8 m, k/4, m/8, t);  COL A (k rows, m contiguous): (4 m, 4 k, m/4, k/4, t)
+      const long long ext_r[5] = {4, 8, g.kseg / 4, g.M / 8, g.nt};
+      const long long str_r[5] = {1, g.lda, 4, 8 * g.lda, g.sA_t};
+      const int box_r[5] = {4, 8, 32 / 4, 128 / 8, 1};
+      const long long ext_c[5] = {4, 4, g.M / 4, g.kseg / 4, g.nt};
+      const long long str_c[5] = {1, g.lda, 4, 4 * g.lda, g.sA_t};
+      const int box_c[5] = {4, 4, 128 / 4, 32 / 4, 1};
       const double* base = g.A[s] + (g.arow ? g.seg_off[j] : 0);
-      if (!make_map64(&tm.A[s * tm.nsegmaps + j], base, g.arow ? ext_r : ext_c, str, g.arow ? 128 : 32,
-                      g.arow ? 4 : 16))
+      if (!make_map64(&tm.A[s * tm.nsegmaps + j], base, g.arow ? ext_r : ext_c, g.arow ? str_r : str_c,
+                      g.arow ? box_r : box_c))
         return false;
     }
-    const long long ext_b[5] = {8, (long long)g.nseg * g.kseg, g.N / 8, g.nt, g.nb};
-    const long long str_b[5] = {1, g.ldb, 8, g.sB_t, g.sB_b};
-    if (!make_map64(&tm.B[s], g.B[s], ext_b, str_b, 32, 16)) return false;
+    // B (k rows, n contiguous): (4 n, 4 k, n/4, k/4, t)
+    const long long ext_b[5] = {4, 4, g.N / 4, (long long)g.nseg * g.kseg / 4, g.nt};
+    const long long str_b[5] = {1, g.ldb, 4, 4 * g.ldb, g.sB_t};
+    const int box_b[5] = {4, 4, 128 / 4, 32 / 4, 1};
+    if (!make_map64(&tm.B[s], g.B[s], ext_b, str_b, box_b)) return false;
   }
   return true;
 }
