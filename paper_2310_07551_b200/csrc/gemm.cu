@@ -1108,7 +1108,9 @@ bool build_tma(const GemmArgs& g, TmaMaps& tm) {
   // long-K launches, >= 32 k-tiles per tile).  Measured per launch (ncu, one step, conflict-free
   // fragment-ordered boxes): C2 DMMA active 92.4 -> 93.4% (first mode, K = 1024), 88.7 -> 89.2%
   // (D2 / D3 first modes), 91.7 -> 93.5% (stage GEMMs, K = 2048 / 4096); C2 2.618 -> 2.579
-  // ms/step.  The short-K (K = 128: 4 k-tiles per tile) C3 launches lose up to 5% with it.
+  // ms/step.  Below 32 k-tiles per tile it does not pay in the live step graphs: the C3 short-K
+  // COL launches (4 k-tiles) lose up to 5% and, with the ROW stage GEMMs (12 / 24 k-tiles) on
+  // TMA too, a C3 step is 1.715 vs 1.710 ms.
   static const int mode = [] {
     const char* e = getenv("KX_GEMM_TMA");
     return e ? atoi(e) : -1;
