@@ -131,6 +131,7 @@ struct Tf32GemmArgs {
   CUtensorMap mapS_hi, mapS_lo, mapT;   // 64-B aligned members first
   int kind, M, N, kseg, nseg, slo, ns, nt, nb, vec4;
   int csplit;   // > 1: cluster split-K — the S CTAs of a cluster share one tile's k-tiles
+  int tile0, tile1;   // the launch covers tiles [tile0, tile1) of the z-major tile order
   float alpha, beta;
   long long ldc, ldd, sC_t, sC_b, sD_t, sD_b;
   float* C[MAXS];
@@ -159,8 +160,8 @@ __device__ __forceinline__ TileCoord tile_coord(const Tf32GemmArgs& p, int tiles
   return c;
 }
 
-// Work items of a CTA: persistent over tiles (whole k range), or — cluster split-K — the one
-// tile of its cluster and its 1/S share of the k-tiles.
+// Work items of a CTA in tiles [tile0, tile1): persistent over tiles (whole k range), or —
+// cluster split-K — the one tile of its cluster and its 1/S share of the k-tiles.
 template <bool SPLIT>
 struct Work {
   int n, tl0, step, kb, ke;
@@ -168,14 +169,15 @@ struct Work {
     if (SPLIT) {
       const int r = blockIdx.x % p.csplit;
       n = 1;
-      tl0 = blockIdx.x / p.csplit;
+      tl0 = p.tile0 + blockIdx.x / p.csplit;
       step = 1;
       kb = r * ktiles / p.csplit;
       ke = (r + 1) * ktiles / p.csplit;
     } else {
-      tl0 = blockIdx.x;
+      tl0 = p.tile0 + blockIdx.x;
       step = gridDim.x;
-      n = tl0 < ntiles ? (ntiles - 1 - tl0) / step + 1 : 0;
+      const int end = min(ntiles, p.tile1);
+      n = tl0 < end ? (end - 1 - tl0) / step + 1 : 0;
       kb = 0;
       ke = ktiles;
     }
@@ -554,40 +556,62 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
   if (e != cudaSuccess) return e;
   const long long tiles = (long long)((g.M + TBM - 1) / TBM) * ((g.N + TBN - 1) / TBN) * g.ns * g.nt * g.nb;
   const int nsm = num_sms_tf32();
-  const int grid = (int)std::min<long long>(tiles, nsm);
-  // few tiles (small grids: the stage GEMMs of a 300^2 step have 18): cluster split-K over S CTAs
-  // per tile, the partials reduced through distributed shared memory
   const int ktiles = (g.kseg + TBK - 1) / TBK * g.nseg;
   static const bool no_split = getenv("KX_TF32_NOSPLIT") != nullptr;   // diagnostics only
-  int S = 0;
-  if (!no_split && tiles * 2 <= nsm && ktiles >= 4) {
-    S = 8;
-    while (S > 1 && (tiles * S > nsm || ktiles < 2 * S)) S /= 2;
-  }
-  p.csplit = S >= 2 ? S : 0;
-  static const bool trace = getenv("KX_TRACE") != nullptr;   // diagnostics only
-  if (trace)
-    fprintf(stderr, "kx-tf32 %s M=%d N=%d K=%dx%d z=%dx%dx%d tiles=%lld grid=%d csplit=%d\n",
-            g.kind == TF32_COL ? "col" : "row", g.M, g.N, g.kseg, g.nseg, g.ns, g.nt, g.nb, tiles, grid, p.csplit);
-  if (p.csplit) {
+  static const bool trace = getenv("KX_TRACE") != nullptr;            // diagnostics only
+  // cluster split-K factor for `t` tiles sharing the SMs (2, 4, 8; 0 = none)
+  auto split_of = [&](long long t, int min_kt) {   // >= min_kt k-tiles per split CTA
+    if (no_split || t * 2 > nsm || ktiles < 2 * min_kt) return 0;
+    int S = 8;
+    while (S > 1 && (t * S > nsm || ktiles < min_kt * S)) S /= 2;
+    return S >= 2 ? S : 0;
+  };
+  auto launch_split = [&](long long t0, long long t1, int S) -> bool {
+    p.csplit = S;
+    p.tile0 = (int)t0;
+    p.tile1 = (int)t1;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(tiles * p.csplit));
+    cfg.gridDim = dim3((unsigned)((t1 - t0) * S));
     cfg.blockDim = dim3(T_THREADS);
     cfg.dynamicSmemBytes = T_SMEM;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.csplit;
+    attr[0].val.clusterDim.x = S;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<true>, p) == cudaSuccess) return cudaSuccess;
-    cudaGetLastError();   // refused (cluster residency): the persistent schedule
+    if (cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<true>, p) == cudaSuccess) return true;
+    cudaGetLastError();   // refused (cluster residency)
+    return false;
+  };
+  auto launch_persistent = [&](long long t0, long long t1) {
     p.csplit = 0;
+    p.tile0 = (int)t0;
+    p.tile1 = (int)t1;
+    tf32x3_gemm_kernel<false><<<(int)std::min<long long>(t1 - t0, nsm), T_THREADS, T_SMEM, stream>>>(p);
+    return cudaGetLastError();
+  };
+  // few tiles (small grids: the stage GEMMs of a 300^2 step have 18): every tile split over a
+  // cluster; many tiles with a short last wave (768 = 5 x 148 + 28 at C2): the whole waves
+  // persistent, then the tail tiles split over clusters (an S-times shorter last wave)
+  // (the tail split pays only with >= 8 k-tiles per split CTA: at K = 128 (C3) it cost 12%)
+  const int S_all = split_of(tiles, 2);
+  const long long tail = tiles > nsm ? tiles % nsm : 0;
+  const int S_tail = tail ? split_of(tail, 8) : 0;
+  if (trace)
+    fprintf(stderr, "kx-tf32 %s M=%d N=%d K=%dx%d z=%dx%dx%d tiles=%lld split=%d tail=%lld split_tail=%d\n",
+            g.kind == TF32_COL ? "col" : "row", g.M, g.N, g.kseg, g.nseg, g.ns, g.nt, g.nb, tiles, S_all, tail,
+            S_tail);
+  if (S_all && launch_split(0, tiles, S_all)) return cudaSuccess;
+  if (S_tail) {
+    e = launch_persistent(0, tiles - tail);
+    if (e != cudaSuccess) return e;
+    if (launch_split(tiles - tail, tiles, S_tail)) return cudaSuccess;
+    return launch_persistent(tiles - tail, tiles);
   }
-  tf32x3_gemm_kernel<false><<<grid, T_THREADS, T_SMEM, stream>>>(p);
-  return cudaGetLastError();
+  return launch_persistent(0, tiles);
 }
 
 }  // namespace kx
