@@ -54,7 +54,7 @@ def make_group(kx, n, P, ncomp=1):
 
 
 @pytest.mark.parametrize("case", [([64, 48], 2), ([128, 96], 4), ([24, 20, 32], 2), ([16, 12, 16], 4),
-                                  ([36, 20, 28], 2), ([8, 6, 5, 4], 2)])
+                                  ([36, 20, 28], 2), ([8, 6, 5, 4], 2), ([64, 24, 32], 8), ([128, 64], 8)])
 def test_tucker_group(kx, case):
     n, P = case
     N = int(np.prod(n))
