@@ -227,3 +227,42 @@ def test_f32_no_out_of_bounds_writes(kx, n):
         assert len(set(v)) == 1, "guard band overwritten"
     assert all(bool(torch.isfinite(u).all()) for u in U)
     ctx.close()
+
+
+def test_step_f32_c4_size_closed_form(kx):
+    """configs[3] size (512^3, FHN delta_v, tau = 0.015) in fp32: g = 0 and cosine-mode data make
+    one exprk3ds_real step the scalar recurrence of Table 3 (as the fp64 test at this size); the
+    fp32 bar: the rounding of the stencil F = K U, amplified by ||K|| / |lambda| (~20 here), and the
+    split products, well inside 1e-4 relative."""
+    import cmath
+    import math
+    from oracle import coeffs
+    n, delta, tau = 512, 42.1887, 0.015
+    A = inputs.laplacian_neumann(n, math.pi, delta)
+    ks = (2, 37, 130)
+    x = inputs.kron_vec([inputs.cosine_mode(n, k) for k in ks])
+    lams = [inputs.cosine_eigenvalue(n, math.pi, delta, k) for k in ks]
+    ctx = kx.Context(0)
+    ctx.set_grid([n, n, n], 2)
+    for c in range(2):
+        for mu in (1, 2, 3):
+            ctx.set_direction_matrix(c, mu, A)
+    ctx.set_model("fhn", inputs.FHN)
+    ctx.set_model("none")
+    ctx.set_tau(tau, "etd3rkds")
+    U = [dev32(x), dev32(x)]
+    ctx.step_f32(U, 1)
+    ctx.sync()
+    s = coeffs.table3(1, 3)
+
+    def phis(ell, z):
+        e = cmath.exp(z)
+        return [e, (e - 1) / z, (e - 1 - z) / (z * z)][ell]
+
+    split = sum(eta * np.prod([phis(li, tau * al[m] * lams[m]) for m in range(3)])
+                for eta, li, al in zip(s.etas, s.inner, s.alphas))
+    expect = np.real(1.0 + tau * sum(lams) * split) * x
+    got = U[0].cpu().numpy().astype(np.float64)
+    err = np.max(np.abs(got - expect)) / np.max(np.abs(expect))
+    assert err <= 1e-4, err
+    ctx.close()
