@@ -266,3 +266,37 @@ def test_step_f32_c4_size_closed_form(kx):
     err = np.max(np.abs(got - expect)) / np.max(np.abs(expect))
     assert err <= 1e-4, err
     ctx.close()
+
+
+@pytest.mark.parametrize("n", [[4, 4], [4, 8, 4], [8], [4, 4, 4, 4]])
+def test_tucker_f32_tiny_and_any_d(kx, n):
+    """Degenerate sizes (the smallest extents the 16-B TMA rows allow, d = 1 and d = 4): every tile
+    is almost all padding, zero-filled by TMA out-of-bounds fill."""
+    N = int(np.prod(n))
+    x = f32(inputs.uniform_sym(101, 0, N))
+    Ls = [f32(inputs.uniform_sym(102, mu, m * m).reshape(m, m)) for mu, m in enumerate(n)]
+    ctx = kx.Context(0)
+    ctx.set_grid(n, 1)
+    Y = dev32(np.zeros(N))
+    ctx.tucker_f32(dev32(x), Y, [col32(L) for L in Ls])
+    ref = vec(tucker(unvec(x.astype(np.float64), n), [L.astype(np.float64) for L in Ls]))
+    assert relerr(Y.cpu().numpy(), ref) <= tucker_tol(n)
+    ctx.close()
+
+
+def test_step_f32_zero_steps_is_noop(kx):
+    prob = inputs.make_problem("schnakenberg", 2, 16, seed=1)
+    ctx = kx.Context(0)
+    ctx.set_grid(prob.n, 2)
+    for c in range(2):
+        for mu in range(2):
+            ctx.set_direction_matrix(c, mu + 1, prob.A[c][mu])
+    ctx.set_model(prob.model, prob.params)
+    ctx.set_tau(1e-4, "etd3rkds")
+    U = [dev32(u) for u in prob.U0]
+    before = [u.clone() for u in U]
+    ctx.step_f32(U, 0)
+    ctx.sync()
+    assert all(torch.equal(a, b) for a, b in zip(U, before))
+    assert ctx.counters()["steps"] == 0
+    ctx.close()
