@@ -23,6 +23,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -253,16 +254,40 @@ def hbm_peak():
         return h, "tools/peaks.cu copy kernel (this job)"
 
 
-def elementwise_roofline(prof):
+def stream_floor(N):
+    """Size floor of HBM streaming at N doubles per field (profiles/stream_probe_r02.log, written
+    by tools/stream_probe.cu on a B200): the step's elementwise launches at C2 are one fused
+    first phase (2 fields read, 4 written) and two D = g(U_s) - G passes (4 read, 2 written);
+    returns their summed bytes / summed floor times in GB/s, or None."""
+    best = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "stream_probe_r02.log")) as f:
+            for line in f:
+                m = re.match(r"N=(\d+) R=(\d+) W=(\d+) grid=\d+: ([\d.]+) us", line)
+                if m:
+                    k = (int(m.group(1)), int(m.group(2)), int(m.group(3)))
+                    best[k] = min(best.get(k, 1e30), float(m.group(4)))
+    except OSError:
+        return None
+    if (N, 2, 4) not in best or (N, 4, 2) not in best:
+        return None
+    return 3 * 48.0 * N / (best[(N, 2, 4)] + 2 * best[(N, 4, 2)]) / 1e3
+
+
+def elementwise_roofline(prof, N=None):
     """Aggregate HBM roofline of the non-GEMM kernels (fused G/F pass, D = g(U_s) - G, ...):
-    algorithmic bytes (whole-field reads + writes) / their event-timed duration."""
+    algorithmic bytes (whole-field reads + writes) / their event-timed duration, next to the
+    size floor of a pure streaming kernel of the same traffic at this N."""
     if not prof.get("other_ms") or not prof.get("other_bytes"):
         return None
     peak, src = hbm_peak()
     ach = prof["other_bytes"] / prof["other_ms"] / 1e6
+    floor = stream_floor(N) if N else None
     return {"bound": "hbm", "kernels": "g_kronsum (G = g(U), F = K U + G), nonlinearity D = g(U_s) - G",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak if peak else None,
-            "peak_source": src, "ms_total": prof["other_ms"]}
+            "peak_source": src, "ms_total": prof["other_ms"],
+            "size_floor": floor, "frac_of_size_floor": ach / floor if floor else None,
+            "size_floor_source": "profiles/stream_probe_r02.log (tools/stream_probe.cu)"}
 
 
 def load_traffic(cfg_name):
@@ -1004,7 +1029,7 @@ def main():
                      "gemm_share_of_step": prof["gemm_ms"] / (res["prof_ms"] * args.steps),
                      "instrumented_ms_per_step": res["prof_ms"],
                      "gemm_launches_per_step": gemm_launches / args.steps},
-        "elementwise_roofline": elementwise_roofline(prof),
+        "elementwise_roofline": elementwise_roofline(prof, int(np.prod(prob.n))),
         "step_tflops": step_flops / res["ms"] / 1e9,
         "gpu_launches": launches,
         "clocks": res["clocks"],

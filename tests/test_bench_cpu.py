@@ -63,3 +63,15 @@ def test_child_env_drops_agent_store(monkeypatch):
     assert "TORCHELASTIC_USE_AGENT_STORE" not in env
     assert env["RANK"] == "1" and env["WORLD_SIZE"] == "2" and env["MASTER_PORT"] == "12345"
     assert env["MASTER_ADDR"] == "127.0.0.1"
+
+
+def test_stream_floor_reads_the_committed_probe():
+    """elementwise_roofline.size_floor: the C2 / C3 floors come from profiles/stream_probe_r02.log
+    (one R2W4 + two R4W2 launches), between the probe's own per-shape rates; unknown N -> None."""
+    sys.path.insert(0, ROOT)
+    import bench
+    f2, f3 = bench.stream_floor(1 << 20), bench.stream_floor(1 << 21)
+    assert 3000 < f2 < 4500 and 4000 < f3 < 6000 and f2 < f3
+    assert bench.stream_floor(12345) is None
+    r = bench.elementwise_roofline({"other_ms": 1.0, "other_bytes": 1e-3 * f2 * 1e9 * 0.5}, 1 << 20)
+    assert abs(r["frac_of_size_floor"] - 0.5) < 1e-9
