@@ -158,6 +158,45 @@ def test_phi_bank_vs_oracle(ctx, case):
     assert worst <= 1e-11, worst
 
 
+def _phi_pade(X, ell):
+    """phi_ell(X) by the block (Van Loan) exponential, computed with scipy's Pade-13 scaling and
+    squaring: expm([[X, I, 0], [0, 0, I], [0, 0, 0]]) holds phi_1(X) / phi_2(X) in its first block
+    row (P:619-625 defines the phi-functions; a different algorithm family from both the
+    library's and the oracle's Taylor + doubling)."""
+    from scipy.linalg import expm
+    n = X.shape[0]
+    if ell == 0:
+        return expm(X)
+    W = np.zeros(((ell + 1) * n, (ell + 1) * n))
+    W[:n, :n] = X
+    for k in range(ell):
+        W[k * n:(k + 1) * n, (k + 1) * n:(k + 2) * n] = np.eye(n)
+    return expm(W)[:n, ell * n:(ell + 1) * n]
+
+
+@pytest.mark.parametrize("case", [("schnakenberg", 2, 64, 1.0 / 3000), ("fhn", 3, 65, 0.015),
+                                  ("schnakenberg", 2, 1024, 2.0 / 6000)],
+                         ids=["schnakenberg64", "fhn65", "C2_1024"])
+def test_phi_bank_vs_pade(ctx, case):
+    """The GPU phi-bank against a Pade-based phi (not Taylor): every matrix at the small sizes,
+    one phi_1 and one phi_2 matrix of each species at the full C2 size."""
+    model, d, n, tau = case
+    prob = inputs.make_problem(model, d, n)
+    setup_problem(ctx, prob, "etd3rkds", tau)
+    s = {1: coeffs.etd3_scheme(1, d), 2: coeffs.etd3_scheme(2, d)}
+    cs = {0: 1 / 3, 1: 2 / 3, 2: 1.0}
+    entries = [(c, ell, stage, i, mu) for c in range(2) for (ell, stage) in [(1, 0), (1, 1), (1, 2), (2, 1), (2, 2)]
+               for i in range(s[ell].nterms) for mu in range(1, d + 1)]
+    if n > 200:   # full size: the first term of each scheme part at the full step, both species
+        entries = [(c, ell, 2, 0, 1) for c in range(2) for ell in (1, 2)]
+    worst = 0.0
+    for (c, ell, stage, i, mu) in entries:
+        P = ctx.phi_matrix(c, ell, stage, i, mu)
+        X = cs[stage] * tau * s[ell].alphas[i][mu - 1] * prob.A[c][mu - 1]
+        worst = max(worst, relerr(P, _phi_pade(X, s[ell].inner[i])))
+    assert worst <= 1e-11, worst
+
+
 @pytest.mark.parametrize("case", [("schnakenberg", 2, 64, 1.0 / 3000), ("fhn", 3, 24, 0.015),
                                   ("schnakenberg", 2, 100, 1e-3)])
 def test_phi_apply_parity(ctx, case):
