@@ -152,7 +152,12 @@ kx_status kx_step(kx_ctx *ctx, double t, double *const *U);
  * replayed nsteps times.  With the NaN watchdog on, steps are launched one by one. */
 kx_status kx_step_n(kx_ctx *ctx, double t0, int nsteps, double *const *U);
 /* Same as kx_step but U are HOST buffers (N doubles each): copies them to the device,
- * steps `nsteps` times (as kx_step_n), copies back, synchronises (end-to-end entry point). */
+ * steps `nsteps` times (as kx_step_n), copies back, synchronises (end-to-end entry point).
+ * With page-locked buffers (cudaHostAlloc / cudaHostRegister / torch pin_memory) the last
+ * step's final stage GEMM runs in 4 row chunks (KX_TAIL_CHUNKS=1..8) and each chunk's rows are
+ * copied back while the next chunk computes.  The result then equals kx_step_n up to the
+ * rounding of that GEMM's split K sums (~1e-16 relative).  It stays deterministic run to run.
+ * Pageable buffers are copied after the last step, bitwise as kx_step_n. */
 kx_status kx_integrate_host(kx_ctx *ctx, double t0, int nsteps, double *const *U_host);
 /* Small 2-D grids (d = 2, 8 <= n_2 <= 64, n_1 <= 64, tridiagonal A_mu, real scheme, one GPU):
  * on = 1 (default) executes each step as ONE kernel on an 8-CTA thread-block cluster that

@@ -84,6 +84,9 @@ void kx_destroy(kx_ctx* c) {
   if (c->nccl_comm && nccl().ok) nccl().CommDestroy(static_cast<ncclComm_t>(c->nccl_comm));
 #endif
   if (c->comm) cudaStreamDestroy(c->comm);
+  if (c->copy) cudaStreamDestroy(c->copy);
+  for (auto e : c->ev_tail)
+    if (e) cudaEventDestroy(e);
   for (auto e : c->ev_term)
     if (e) cudaEventDestroy(e);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -592,9 +595,27 @@ kx_status kx_integrate_host(kx_ctx* c, double t0, int nsteps, double* const* U_h
     KX_CUDA(c, cudaMemcpyAsync(c->hostU[s], U_host[s], bytes, cudaMemcpyHostToDevice, c->stream));
   }
   (void)t0;
-  KX_TRY(steps_impl(c, c->hostU, nsteps));
-  for (int s = 0; s < c->ncomp; ++s)
-    KX_CUDA(c, cudaMemcpyAsync(U_host[s], c->hostU[s], bytes, cudaMemcpyDeviceToHost, c->stream));
+  // the last step's final stage GEMM in row chunks, each chunk's rows copied back while the
+  // next one computes (final_concat); KX_TAIL_CHUNKS=1 / profiling: copy after the last step
+  static const int chunks = [] {
+    const char* e = getenv("KX_TAIL_CHUNKS");
+    return e ? std::max(1, std::min(atoi(e), kTailMaxChunks)) : 4;
+  }();
+  c->tail_chunks = chunks;
+  bool pinned = true;   // graph-captured copies need page-locked host buffers
+  for (int s = 0; s < c->ncomp && pinned; ++s) {
+    cudaPointerAttributes at{};
+    pinned = cudaPointerGetAttributes(&at, U_host[s]) == cudaSuccess && at.type == cudaMemoryTypeHost;
+  }
+  cudaGetLastError();
+  if (nsteps >= 1 && chunks > 1 && !c->profiling && pinned) {
+    KX_TRY(steps_impl(c, c->hostU, nsteps - 1));
+    KX_TRY(tail_step_impl(c, c->hostU, U_host));
+  } else {
+    KX_TRY(steps_impl(c, c->hostU, nsteps));
+    for (int s = 0; s < c->ncomp; ++s)
+      KX_CUDA(c, cudaMemcpyAsync(U_host[s], c->hostU[s], bytes, cudaMemcpyDeviceToHost, c->stream));
+  }
   KX_CUDA(c, cudaStreamSynchronize(c->stream));
   return KX_OK;
 }

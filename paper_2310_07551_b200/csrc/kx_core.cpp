@@ -68,6 +68,7 @@ void free_list(std::vector<double*>& v) {
 
 void drop_graph(kx_ctx* c) {
   f32_drop_graph(c);
+  drop_tail_graph(c);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   c->gexec = nullptr;
@@ -327,13 +328,15 @@ kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* c
 
 // Last mode (mu = 1) with concatenated K over `nseg` slots of ws (or over the single input
 // tensor src when d == 1):  Y_s = alpha * sum_k Wslot_k x_1 Bblock_k + beta * Dd_s.
-kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
-                           const int* slots, double* const* B, double* const* Y, double alpha,
-                           double beta, const double* const* Dd) {
+namespace {
+// rows [r0, r1) of the concatenated-K last-mode GEMM (row = one i_1 line of the output)
+kx_status concat_rows(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
+                      const int* slots, double* const* B, double* const* Y, double alpha,
+                      double beta, const double* const* Dd, long long r0, long long r1) {
   const long long n1 = c->tn[0];
   GemmArgs g;
   g.arow = true;
-  g.M = (int)(c->tN / n1);
+  g.M = (int)(r1 - r0);
   g.N = (int)n1;
   g.kseg = (int)n1;
   g.nseg = nseg;
@@ -345,14 +348,42 @@ kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* sr
   g.alpha = alpha;
   g.beta = beta;
   for (int k = 0; k < nseg; ++k) g.seg_off[k] = ws ? (long long)slots[k] * c->tN : 0;
+  const long long off = r0 * n1;
   for (int s = 0; s < c->ncomp; ++s) {
-    g.A[s] = ws ? ws[s] : src[s];
+    g.A[s] = (ws ? ws[s] : src[s]) + off;
     g.B[s] = B[s];
-    g.C[s] = Y[s];
-    g.D[s] = (Dd && beta != 0.0) ? Dd[s] : nullptr;
+    g.C[s] = Y[s] + off;
+    g.D[s] = (Dd && beta != 0.0) ? Dd[s] + off : nullptr;
   }
-  KX_TRY(run_gemm(c, g));
+  return run_gemm(c, g);
+}
+}  // namespace
+
+kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
+                           const int* slots, double* const* B, double* const* Y, double alpha,
+                           double beta, const double* const* Dd) {
+  KX_TRY(concat_rows(c, ws, src, nseg, slots, B, Y, alpha, beta, Dd, 0, c->tN / c->tn[0]));
   c->cnt.mode_products += (long long)c->ncomp * nseg;
+  return KX_OK;
+}
+
+kx_status final_concat(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
+                       const int* slots, double* const* B, double* const* Y, double alpha,
+                       double beta, const double* const* Dd) {
+  if (!c->tail_armed) return last_mode_concat(c, ws, src, nseg, slots, B, Y, alpha, beta, Dd);
+  const long long n1 = c->tn[0], M = c->tN / n1;
+  const int P = (int)std::max<long long>(1, std::min<long long>(std::min(c->tail_chunks, kTailMaxChunks), M));
+  for (int k = 0; k < P; ++k) {
+    const long long r0 = M * k / P, r1 = M * (k + 1) / P;
+    KX_TRY(concat_rows(c, ws, src, nseg, slots, B, Y, alpha, beta, Dd, r0, r1));
+    KX_CUDA(c, cudaEventRecord(c->ev_tail[k], c->cur));
+    KX_CUDA(c, cudaStreamWaitEvent(c->copy, c->ev_tail[k], 0));
+    for (int s = 0; s < c->ncomp; ++s)
+      KX_CUDA(c, cudaMemcpyAsync(c->tail_host[s] + r0 * n1, Y[s] + r0 * n1, (size_t)((r1 - r0) * n1) * 8,
+                                 cudaMemcpyDeviceToHost, c->copy));
+  }
+  c->cnt.mode_products += (long long)c->ncomp * nseg;
+  c->tail_done = true;
   return KX_OK;
 }
 

@@ -83,6 +83,8 @@ using kx::detail::Stage;
 using kx::MAXS;
 using kx::MAXSEG;
 
+constexpr int kTailMaxChunks = 8;
+
 struct kx_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;      // user stream
@@ -132,6 +134,20 @@ struct kx_ctx {
   double* W2[MAXS] = {};
   std::vector<double*> ws_allocs;
   double* hostU[MAXS] = {};
+  // kx_integrate_host: the last step's final stage GEMM runs in row chunks and each chunk's
+  // rows are copied to the host on `copy` while the next chunk computes (one graph, cached per
+  // host buffers and bank version)
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_tail[kTailMaxChunks + 1] = {};   // chunk k done; [kTailMaxChunks]: copies joined
+  int tail_chunks = 4;
+  bool tail_armed = false, tail_done = false;
+  double* tail_host[MAXS] = {};
+  cudaGraph_t tail_graph = nullptr;
+  cudaGraphExec_t tail_gexec = nullptr;
+  double* tail_key[MAXS] = {};   // host buffers the tail graph copies to
+  double* tail_U[MAXS] = {};     // device state it steps
+  long long tail_version = -1;
+  kx_counters tail_delta{};
   int* flag = nullptr;
   double* sk_ws = nullptr;      // stream-K partial tiles (kx::kSkSlots x 128 x 128)
   int* sk_flags = nullptr;      // stream-K flags (zero between launches)
@@ -266,6 +282,11 @@ kx_status group_modes(kx_ctx* c, const Group& G, int t0, int nt, const double* c
 kx_status last_mode_concat(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
                            const int* slots, double* const* B, double* const* Y, double alpha,
                            double beta, const double* const* Dd);
+// the step's final stage GEMM: last_mode_concat, or (c->tail_armed) in row chunks, each copied
+// to c->tail_host on c->copy as soon as it is written
+kx_status final_concat(kx_ctx* c, double* const* ws, const double* const* src, int nseg,
+                       const int* slots, double* const* B, double* const* Y, double alpha,
+                       double beta, const double* const* Dd);
 kx_status nonlin(kx_ctx* c, int mode, const double* const* u, double* const* out);
 kx_status check_ptr(kx_ctx* c, const void* p, const char* what);
 template <class F>
@@ -293,6 +314,8 @@ kx_status enqueue_watch(kx_ctx* c, double* const* U);
 bool fused_eligible(const kx_ctx* c);
 kx_status enqueue_fused(kx_ctx* c, double* const* U, int nsteps);
 kx_status step_impl(kx_ctx* c, double* const* U);
+kx_status tail_step_impl(kx_ctx* c, double* const* U, double* const* U_host);
+void drop_tail_graph(kx_ctx* c);
 // ---- kx_bank.cpp: phi-bank formation
 kx_status set_tau_impl(kx_ctx* c, double tau, kx_scheme scheme);
 kx_status form_block(kx_ctx* c, const std::vector<Group>& groups, const BlockRecipe& r);

@@ -61,8 +61,8 @@ kx_status enqueue_step_etd3(kx_ctx* c, double* const* U) {
   // D3 = g(U3) - G; U+ = U + tau S_1^tau[F] + 3tau/2 S_2^tau[D3]
   KX_TRY(nonlin(c, 1, c->Us, c->D));
   KX_TRY(group_modes(c, c->groups[2], 0, c->groups[2].nterms, c->D, c->groups[2].slot0, &ws));
-  KX_TRY(last_mode_concat(c, ws, nullptr, c->stages[2].nseg, c->stages[2].slot, c->stages[2].B,
-                          U, 1.0, 1.0, U));
+  KX_TRY(final_concat(c, ws, nullptr, c->stages[2].nseg, c->stages[2].slot, c->stages[2].B,
+                      U, 1.0, 1.0, U));
   c->cnt.tucker_ops += (long long)ns * 5 * c->T;   // 3T on F, T on D2, T on D3
   return KX_OK;
 }
@@ -76,7 +76,7 @@ kx_status enqueue_step_etd2(kx_ctx* c, double* const* U) {
   KX_TRY(last_mode_concat(c, ws, c->F, 1, c->stages[0].slot, c->stages[0].B, c->Us, 1.0, 1.0, U));
   KX_TRY(nonlin(c, 1, c->Us, c->D));
   KX_TRY(group_modes(c, c->groups[1], 0, 1, c->D, c->groups[1].slot0, &ws));
-  KX_TRY(last_mode_concat(c, ws, c->D, 1, c->stages[1].slot, c->stages[1].B, U, 1.0, 1.0, c->Us));
+  KX_TRY(final_concat(c, ws, c->D, 1, c->stages[1].slot, c->stages[1].B, U, 1.0, 1.0, c->Us));
   c->cnt.tucker_ops += (long long)ns * 2;
   return KX_OK;
 }
@@ -247,6 +247,82 @@ kx_status step_impl(kx_ctx* c, double* const* U) {
       (r.cls == 0 ? c->prof_flops : c->prof_bytes) += r.flops;
     }
   }
+  return KX_OK;
+}
+
+// ---------------------------------------------------------------- host-buffer tail -------
+void drop_tail_graph(kx_ctx* c) {
+  if (c->tail_gexec) cudaGraphExecDestroy(c->tail_gexec);
+  if (c->tail_graph) cudaGraphDestroy(c->tail_graph);
+  c->tail_gexec = nullptr;
+  c->tail_graph = nullptr;
+  c->tail_version = -1;
+}
+
+// The last step of kx_integrate_host with the device -> host copy of U overlapped with its
+// final stage GEMM (final_concat in row chunks); a plain copy after the step when the step has
+// no such GEMM (the one-kernel small-grid path).  Captured once per (U, U_host, bank) and
+// replayed; the counters advance by one step per replay as in step_impl.
+kx_status tail_step_impl(kx_ctx* c, double* const* U, double* const* U_host) {
+  bool same = c->tail_gexec && c->tail_version == c->bank_version;
+  for (int s = 0; s < c->ncomp && same; ++s) same = c->tail_key[s] == U_host[s] && c->tail_U[s] == U[s];
+  if (!same) {
+    drop_tail_graph(c);
+    if (!c->copy) KX_CUDA(c, cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : c->ev_tail)
+      if (!e) KX_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const kx_counters before = c->cnt;
+    c->cur = c->cap;
+    for (int s = 0; s < c->ncomp; ++s) c->tail_host[s] = U_host[s];
+    c->tail_armed = true;
+    c->tail_done = false;
+    KX_CUDA(c, cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+    kx_status st = enqueue_step(c, U);
+    c->tail_armed = false;
+    const size_t bytes = (size_t)c->tN * 8;
+    if (st == KX_OK && c->tail_done) {   // join the copy stream back into the capture
+      if (cudaEventRecord(c->ev_tail[kTailMaxChunks], c->copy) != cudaSuccess ||
+          cudaStreamWaitEvent(c->cap, c->ev_tail[kTailMaxChunks], 0) != cudaSuccess)
+        st = fail(c, KX_ERR_CUDA, "tail join");
+    } else if (st == KX_OK) {
+      for (int s = 0; s < c->ncomp && st == KX_OK; ++s)
+        if (cudaMemcpyAsync(U_host[s], U[s], bytes, cudaMemcpyDeviceToHost, c->cap) != cudaSuccess)
+          st = fail(c, KX_ERR_CUDA, "tail copy");
+    }
+    cudaGraph_t gr = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(c->cap, &gr);
+    c->cur = c->stream;
+    c->recs.clear();
+    if (st != KX_OK) {
+      if (gr) cudaGraphDestroy(gr);
+      c->cnt = before;
+      return st;
+    }
+    KX_CUDA(c, e);
+    c->tail_graph = gr;
+    KX_CUDA(c, cudaGraphInstantiate(&c->tail_gexec, c->tail_graph, 0));
+    c->tail_version = c->bank_version;
+    for (int s = 0; s < c->ncomp; ++s) c->tail_key[s] = U_host[s], c->tail_U[s] = U[s];
+    kx_counters dl = c->cnt;
+    dl.steps = 0;
+    dl.tucker_ops -= before.tucker_ops;
+    dl.mode_products -= before.mode_products;
+    dl.kronsum_actions -= before.kronsum_actions;
+    dl.phi_builds = 0;
+    dl.gemm_launches -= before.gemm_launches;
+    dl.other_launches -= before.other_launches;
+    dl.mode_product_flops -= before.mode_product_flops;
+    c->tail_delta = dl;
+    c->cnt = before;
+  }
+  KX_CUDA(c, cudaGraphLaunch(c->tail_gexec, c->stream));
+  c->cnt.steps += 1;
+  c->cnt.tucker_ops += c->tail_delta.tucker_ops;
+  c->cnt.mode_products += c->tail_delta.mode_products;
+  c->cnt.kronsum_actions += c->tail_delta.kronsum_actions;
+  c->cnt.gemm_launches += c->tail_delta.gemm_launches;
+  c->cnt.other_launches += c->tail_delta.other_launches;
+  c->cnt.mode_product_flops += c->tail_delta.mode_product_flops;
   return KX_OK;
 }
 

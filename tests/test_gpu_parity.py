@@ -326,6 +326,33 @@ def test_integrate_host_matches_device(ctx):
         assert np.array_equal(Uh[c], Ud[c].cpu().numpy())
 
 
+@pytest.mark.parametrize("case", [("schnakenberg", 2, [160, 96], "etd3rkds"), ("fhn", 3, [24, 20, 16], "etd2rkds"),
+                                  ("schnakenberg", 2, [1024, 1024], "etd3rkds")],
+                         ids=["160x96_etd3", "24x20x16_etd2", "C2_1024"])
+def test_integrate_host_pinned_tail(ctx, case):
+    """kx_integrate_host with page-locked host buffers: the last step's final stage GEMM runs in
+    row chunks whose rows are copied back while the next chunk computes.  Equal to the device
+    path up to the rounding of that GEMM's k-split (<= 1e-14 relative); counters advance by the
+    steps taken; a second call replays the cached graph with the same result."""
+    model, d, n, scheme = case
+    prob = inputs.make_problem(model, d, n, seed=3)
+    tau = 1e-4 if model == "schnakenberg" else 0.01
+    setup_problem(ctx, prob, scheme, tau)
+    Ud = [dev(u) for u in prob.U0]
+    for _ in range(3):
+        ctx.step(Ud)
+    ref = [u.cpu().numpy() for u in Ud]
+    pinned = [torch.from_numpy(u.copy()).pin_memory() for u in prob.U0]
+    for rep in range(2):
+        for c in range(2):
+            pinned[c].copy_(torch.from_numpy(prob.U0[c]))
+        ctx.reset_counters()
+        ctx.integrate_host([p.numpy() for p in pinned], 3)
+        assert ctx.counters()["steps"] == 3
+        for c in range(2):
+            assert relerr(pinned[c].numpy(), ref[c]) <= 1e-14, (rep, c)
+
+
 def test_equilibrium_and_finite(ctx):
     prob = inputs.make_problem("fhn", 3, 16, amplitude=0.0)
     setup_problem(ctx, prob, "etd3rkds", 0.015)
