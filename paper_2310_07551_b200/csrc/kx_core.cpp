@@ -373,8 +373,36 @@ kx_status final_concat(kx_ctx* c, double* const* ws, const double* const* src, i
   if (!c->tail_armed) return last_mode_concat(c, ws, src, nseg, slots, B, Y, alpha, beta, Dd);
   const long long n1 = c->tn[0], M = c->tN / n1;
   const int P = (int)std::max<long long>(1, std::min<long long>(std::min(c->tail_chunks, kTailMaxChunks), M));
+  // shrinking chunks (weights P, P-1, ..., 1): each chunk's copy hides under the next chunk's
+  // GEMM and the last, unhidden copy is the smallest.  Whole 128-row tile rows per chunk
+  // (largest-remainder rounding); grids with fewer tile rows than chunks take one chunk.
+  // Copy-bound tails (the copy of a chunk outlasts the next chunk's GEMM: C3) keep equal chunks.
+  const double copy_us = 8.0 * c->ncomp * (double)c->tN / 50e3;   // ~50 GB/s D2H
+  const double gemm_us = 2.0 * c->ncomp * (double)c->tN * n1 * nseg / 30e6;   // ~30 TF/s
+  const bool shrink = copy_us < gemm_us;
+  const long long TR = (M + 127) / 128, W = shrink ? (long long)P * (P + 1) / 2 : P;
+  long long rows_of[kTailMaxChunks] = {}, used = 0;
+  double rem[kTailMaxChunks];
   for (int k = 0; k < P; ++k) {
-    const long long r0 = M * k / P, r1 = M * (k + 1) / P;
+    const double want = (double)TR * (shrink ? P - k : 1) / (double)W;
+    rows_of[k] = (long long)want;
+    rem[k] = want - (double)rows_of[k];
+    used += rows_of[k];
+  }
+  for (; used < TR; ++used) {
+    int best = 0;
+    for (int k = 1; k < P; ++k)
+      if (rem[k] > rem[best]) best = k;
+    rows_of[best] += 1;
+    rem[best] = -1.0;
+  }
+  long long bound[kTailMaxChunks + 1];
+  bound[0] = 0;
+  for (int k = 0; k < P; ++k) bound[k + 1] = std::min(M, bound[k] + 128 * (TR < P ? (k == 0 ? TR : 0) : rows_of[k]));
+  bound[P] = M;
+  for (int k = 0; k < P; ++k) {
+    const long long r0 = bound[k], r1 = bound[k + 1];
+    if (r1 <= r0) continue;
     KX_TRY(concat_rows(c, ws, src, nseg, slots, B, Y, alpha, beta, Dd, r0, r1));
     KX_CUDA(c, cudaEventRecord(c->ev_tail[k], c->cur));
     KX_CUDA(c, cudaStreamWaitEvent(c->copy, c->ev_tail[k], 0));
