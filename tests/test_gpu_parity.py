@@ -327,8 +327,9 @@ def test_integrate_host_matches_device(ctx):
 
 
 @pytest.mark.parametrize("case", [("schnakenberg", 2, [160, 96], "etd3rkds"), ("fhn", 3, [24, 20, 16], "etd2rkds"),
-                                  ("schnakenberg", 2, [1024, 1024], "etd3rkds")],
-                         ids=["160x96_etd3", "24x20x16_etd2", "C2_1024"])
+                                  ("schnakenberg", 2, [1024, 1024], "etd3rkds"), ("schnakenberg", 2, [48, 40], "etd3rkds"),
+                                  ("fhn", 3, [32, 32, 32], "exprk3ds_cplx")],
+                         ids=["160x96_etd3", "24x20x16_etd2", "C2_1024", "48x40_one_kernel", "32cube_cplx"])
 def test_integrate_host_pinned_tail(ctx, case):
     """kx_integrate_host with page-locked host buffers: the last step's final stage GEMM runs in
     row chunks whose rows are copied back while the next chunk computes.  Equal to the device
