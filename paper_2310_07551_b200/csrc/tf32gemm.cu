@@ -51,6 +51,10 @@ constexpr int T_THREADS = 320;
 constexpr int T_PSTRIDE = TBN + 4;                     // cluster split-K partial row (floats)
 static_assert(TBM * T_PSTRIDE * 4 <= TSTAGES * T_STAGE_BYTES, "partial fits in the stage memory");
 constexpr int T_KBUF = 4;                              // per-k-tile partial accumulators in TMEM
+#ifndef KX_TF32_KPP
+#define KX_TF32_KPP 2
+#endif
+constexpr int T_KPP = KX_TF32_KPP;                     // k-tiles summed in TMEM per partial
 constexpr int T_TMEM_COLS = T_KBUF * TBN;              // 4 x 128 fp32 columns = all of TMEM
 
 __device__ __forceinline__ unsigned su32(const void* p) {
@@ -266,10 +270,17 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
     // ------------------------------------------------------------ MMA issuer
     int it = 0;
     const Work<SPLIT> wk(p, ntiles, ktiles);
+    int pt = 0;   // partials started
     for (int w = 0; w < wk.n; ++w) {
       for (int kt = wk.kb; kt < wk.ke; ++kt, ++it) {
-        const int st = it % TSTAGES, cb = it % TCONV, kb = it % T_KBUF;
-        if (it >= T_KBUF) mbar_wait(kempty + kb, ((it / T_KBUF) - 1) & 1);   // partial read back
+        const int st = it % TSTAGES, cb = it % TCONV;
+        const bool first = (kt - wk.kb) % T_KPP == 0;
+        const bool last = (kt - wk.kb) % T_KPP == T_KPP - 1 || kt + 1 == wk.ke;
+        const int kb = (first ? pt : pt - 1) % T_KBUF;
+        if (first) {
+          if (pt >= T_KBUF) mbar_wait(kempty + kb, ((pt / T_KBUF) - 1) & 1);   // partial read back
+          ++pt;
+        }
         mbar_wait(full + st, (it / TSTAGES) & 1);
         mbar_wait(cfull + cb, (it / TCONV) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -282,13 +293,13 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
           const unsigned b_hi = col ? t_hi : s_hi, b_lo = col ? t_lo : s_lo;
 #pragma unroll
           for (int ks = 0; ks < TBK / 8; ++ks) {   // k-step = 32 B inside the 128-B swizzled rows
-            mma_tf32(tmem_d, sdesc(a_lo + ks * 32), sdesc(b_hi + ks * 32), ks > 0 ? 1u : 0u);
+            mma_tf32(tmem_d, sdesc(a_lo + ks * 32), sdesc(b_hi + ks * 32), (ks > 0 || !first) ? 1u : 0u);
             mma_tf32(tmem_d, sdesc(a_hi + ks * 32), sdesc(b_lo + ks * 32), 1u);
             mma_tf32(tmem_d, sdesc(a_hi + ks * 32), sdesc(b_hi + ks * 32), 1u);
           }
           mma_commit(empty + st);    // static planes free once these MMAs finish
           mma_commit(cempty + cb);   // converted buffer free
-          mma_commit(kfull + kb);    // this k-tile's partial complete
+          if (last) mma_commit(kfull + kb);    // this partial (kpp k-tiles) complete
         }
         __syncwarp();
       }
@@ -348,7 +359,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
       float acc[TBN];
 #pragma unroll
       for (int j = 0; j < TBN; ++j) acc[j] = 0.0f;
-      for (int kt = wk.kb; kt < wk.ke; ++kt, ++it) {
+      for (int kt = wk.kb; kt < wk.ke; kt += T_KPP, ++it) {   // it: partials read back
         const int kb = it % T_KBUF;
         mbar_wait(kfull + kb, (it / T_KBUF) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
