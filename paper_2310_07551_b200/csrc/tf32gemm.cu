@@ -137,6 +137,7 @@ struct Tf32GemmArgs {
   int csplit;   // > 1: cluster split-K — the S CTAs of a cluster share one tile's k-tiles
   int tile0, tile1;   // the launch covers tiles [tile0, tile1) of the z-major tile order
   float alpha, beta;
+  int diag_nostore;   // diagnostics (KX_TF32_NOSTORE=1): skip the output stores
   long long ldc, ldd, sC_t, sC_b, sD_t, sD_b;
   float* C[MAXS];
   const float* D[MAXS];
@@ -414,7 +415,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
         continue;
       }
       const int m = c.m0 + q * 32 + lane;
-      if (m >= p.M) continue;
+      if (m >= p.M || p.diag_nostore) continue;
       const long long oc = c.t * p.sC_t + c.b * p.sC_b + (long long)m * p.ldc + c.n0;
       const long long od = c.t * p.sD_t + c.b * p.sD_b + (long long)m * p.ldd + c.n0;
       float* C = p.C[c.s];
@@ -559,6 +560,8 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
       vec4 = vec4 && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
   }
   p.vec4 = vec4;
+  static const int nostore = getenv("KX_TF32_NOSTORE") ? 1 : 0;
+  p.diag_nostore = nostore;
   const int mS = g.kind == TF32_COL ? TBM : TBN;   // static operand rows per tile
   if ((e = make_map(&p.mapS_hi, g.S.hi, g.S, TBK, mS, true)) != cudaSuccess) return e;
   if ((e = make_map(&p.mapS_lo, g.S.lo, g.S, TBK, mS, true)) != cudaSuccess) return e;
