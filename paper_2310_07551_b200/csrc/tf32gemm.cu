@@ -46,7 +46,9 @@ constexpr int TBM = 128, TBN = 128, TBK = 32, TSTAGES = 3, TCONV = 2;
 constexpr int T_PLANE = 128 * TBK * 4;                 // 16 KB: one 128 x 32 fp32 tile
 constexpr int T_STAGE_BYTES = 3 * T_PLANE;             // static hi, static lo, raw tensor
 constexpr int T_CONV_BYTES = 2 * T_PLANE;              // converted tensor hi, lo
-constexpr int T_SMEM = TSTAGES * T_STAGE_BYTES + TCONV * T_CONV_BYTES + 1024 /* alignment */ + 256;
+constexpr int T_EPI_BYTES = 4 * 32 * 32 * 4;            // per epilogue warp: one 32 x 32 fp32 store chunk
+// stages | converted buffers | barriers (1 KB block) | epilogue store chunks (1 KB aligned) + alignment
+constexpr int T_SMEM = TSTAGES * T_STAGE_BYTES + TCONV * T_CONV_BYTES + 1024 + T_EPI_BYTES + 1024;
 constexpr int T_THREADS = 320;
 constexpr int T_PSTRIDE = TBN + 4;                     // cluster split-K partial row (floats)
 static_assert(TBM * T_PSTRIDE * 4 <= TSTAGES * T_STAGE_BYTES, "partial fits in the stage memory");
@@ -88,6 +90,15 @@ __device__ __forceinline__ void tma_load5(void* dst, const CUtensorMap* map, int
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(su32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(su32(bar))
       : "memory");
+}
+
+// tiled TMA store of a shared-memory box (5-D map, bulk-group completion)
+__device__ __forceinline__ void tma_store5(const CUtensorMap* map, const void* src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(0)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
 
 // shared-memory matrix descriptor (tcgen05), K-major, 128-B swizzle: start, leading / stride
@@ -133,11 +144,13 @@ __device__ __forceinline__ void split4(const float4 x, float4& h, float4& l) {
 
 struct Tf32GemmArgs {
   CUtensorMap mapS_hi, mapS_lo, mapT;   // 64-B aligned members first
+  CUtensorMap mapC[MAXS];               // output (n, m, t, b), 32 x 32 boxes, 128-B swizzle (tma_store)
   int kind, M, N, kseg, nseg, slo, ns, nt, nb, vec4;
   int csplit;   // > 1: cluster split-K — the S CTAs of a cluster share one tile's k-tiles
   int tile0, tile1;   // the launch covers tiles [tile0, tile1) of the z-major tile order
   float alpha, beta;
   int diag_nostore;   // diagnostics (KX_TF32_NOSTORE=1): skip the output stores
+  int tma_store;      // 1: whole-chunk TMA stores of the output (mapC), else per-thread rows
   long long ldc, ldd, sC_t, sC_b, sD_t, sD_b;
   float* C[MAXS];
   const float* D[MAXS];
@@ -206,6 +219,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
   uint64_t* kfull = cempty + TCONV;     // k-tile partial ready (MMA -> accumulator warps)
   uint64_t* kempty = kfull + T_KBUF;    // partial read back (accumulator warps -> MMA)
   unsigned* tmem_slot = reinterpret_cast<unsigned*>(kempty + T_KBUF);
+  float* epi = reinterpret_cast<float*>(conv + TCONV * T_CONV_BYTES + 1024);   // 1 KB aligned store chunks
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (p.M + TBM - 1) / TBM, tiles_n = (p.N + TBN - 1) / TBN;
@@ -414,12 +428,48 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
         cl.sync();   // no CTA leaves while its partial may still be read
         continue;
       }
+      if (p.diag_nostore) continue;
       const int m = c.m0 + q * 32 + lane;
-      if (m >= p.M || p.diag_nostore) continue;
       const long long oc = c.t * p.sC_t + c.b * p.sC_b + (long long)m * p.ldc + c.n0;
       const long long od = c.t * p.sD_t + c.b * p.sD_b + (long long)m * p.ldd + c.n0;
       float* C = p.C[c.s];
       const float* D = p.D[c.s];
+      if (p.tma_store) {
+        // this warp's 32 rows go out as four 32 x 32 boxes: each thread writes its row's 32
+        // values into the 128-B-swizzled chunk (16-B pieces XOR row: conflict-free), one lane
+        // issues the TMA store; the chunk is rewritten only after that store has read it.
+        // Out-of-range rows / columns are clipped by the TMA unit.
+        float* stg = epi + q * (32 * 32);
+        const bool dl = D && m < p.M;
+#pragma unroll
+        for (int cb = 0; cb < TBN; cb += 32) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[cb + j] *= p.alpha;   // in place: no extra registers
+          if (dl) {   // tma_store implies vec4: a float4 of D is wholly inside or outside N
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (c.n0 + cb + 4 * j < p.N) {
+                const float4 dd = *reinterpret_cast<const float4*>(D + od + cb + 4 * j);
+                acc[cb + 4 * j] += p.beta * dd.x;
+                acc[cb + 4 * j + 1] += p.beta * dd.y;
+                acc[cb + 4 * j + 2] += p.beta * dd.z;
+                acc[cb + 4 * j + 3] += p.beta * dd.w;
+              }
+            }
+          }
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(stg + lane * 32 + ((j ^ (lane & 7)) << 2)) =
+                make_float4(acc[cb + 4 * j], acc[cb + 4 * j + 1], acc[cb + 4 * j + 2], acc[cb + 4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store5(&p.mapC[c.s], stg, c.n0 + cb, c.m0 + q * 32, c.t, c.b);
+        }
+        continue;
+      }
+      if (m >= p.M) continue;
       if (c.n0 + TBN <= p.N && p.vec4) {
 #pragma unroll
         for (int j = 0; j < TBN; j += 4) {
@@ -445,6 +495,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
       }
     }
   }
+  if (!SPLIT && warp >= 6 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   if (SPLIT && warp < 6) {   // the epilogue warps' two cluster barriers, joined by all
     namespace cg = cooperative_groups;
     cg::this_cluster().sync();
@@ -562,6 +613,19 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
   p.vec4 = vec4;
   static const int nostore = getenv("KX_TF32_NOSTORE") ? 1 : 0;
   p.diag_nostore = nostore;
+  static const bool no_tma_store = getenv("KX_TF32_ROWSTORE") != nullptr;   // A/B experiments only
+  p.tma_store = 0;
+  if (!no_tma_store) {
+    bool ok = true;
+    for (int s = 0; s < g.ns && ok; ++s) {
+      Tf32Dim dc;
+      dc.hi = g.C[s];
+      dc.ext[0] = g.N, dc.ext[1] = g.M, dc.ext[2] = g.nt, dc.ext[3] = g.nb;
+      dc.stride[1] = g.ldc, dc.stride[2] = g.sC_t, dc.stride[3] = g.sC_b;
+      ok = (reinterpret_cast<uintptr_t>(g.C[s]) & 15) == 0 && make_map(&p.mapC[s], g.C[s], dc, 32, 32, true) == cudaSuccess;
+    }
+    p.tma_store = ok && vec4 ? 1 : 0;
+  }
   const int mS = g.kind == TF32_COL ? TBM : TBN;   // static operand rows per tile
   if ((e = make_map(&p.mapS_hi, g.S.hi, g.S, TBK, mS, true)) != cudaSuccess) return e;
   if ((e = make_map(&p.mapS_lo, g.S.lo, g.S, TBK, mS, true)) != cudaSuccess) return e;

@@ -92,6 +92,7 @@ def test_fp32_gemm_is_tcgen05_with_tma(sass):
         assert "LDTM" in f
         assert "DMMA" not in f
     assert any("UCGABAR" in f for f in fs)   # the split variant's cluster barriers
+    assert any("UTMASTG" in f for f in fs)   # the persistent variant's TMA output stores
 
 
 def test_peer_store_gemms_fence_at_system_scope(sass):
