@@ -101,6 +101,17 @@ __device__ __forceinline__ void tma_store5(const CUtensorMap* map, const void* s
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
 }
 
+// the same box added element-wise into global memory (TMA reduction, fp32 add, round to nearest)
+__device__ __forceinline__ void tma_reduce_add5(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                int c3) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.5d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(su32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(0)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+
 // shared-memory matrix descriptor (tcgen05), K-major, 128-B swizzle: start, leading / stride
 // byte offsets (16-B units), version 1 (sm_100), layout SWIZZLE_128B
 __device__ __forceinline__ uint64_t sdesc(unsigned saddr) {
@@ -150,7 +161,8 @@ struct Tf32GemmArgs {
   int tile0, tile1;   // the launch covers tiles [tile0, tile1) of the z-major tile order
   float alpha, beta;
   int diag_nostore;   // diagnostics (KX_TF32_NOSTORE=1): skip the output stores
-  int tma_store;      // 1: whole-chunk TMA stores of the output (mapC), else per-thread rows
+  int tma_store;      // 1: whole-chunk TMA stores of the output (mapC), else per-thread rows;
+                      // 2: in place C += alpha acc (C == D, beta == 1) as TMA reduce-add boxes
   long long ldc, ldd, sC_t, sC_b, sD_t, sD_b;
   float* C[MAXS];
   const float* D[MAXS];
@@ -440,7 +452,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
         // issues the TMA store; the chunk is rewritten only after that store has read it.
         // Out-of-range rows / columns are clipped by the TMA unit.
         float* stg = epi + q * (32 * 32);
-        const bool dl = D && m < p.M;
+        const bool dl = D && m < p.M && p.tma_store == 1;
 #pragma unroll
         for (int cb = 0; cb < TBN; cb += 32) {
 #pragma unroll
@@ -465,7 +477,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) tf32x3_gemm_kernel(const __grid_
                 make_float4(acc[cb + 4 * j], acc[cb + 4 * j + 1], acc[cb + 4 * j + 2], acc[cb + 4 * j + 3]);
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           __syncwarp();
-          if (lane == 0) tma_store5(&p.mapC[c.s], stg, c.n0 + cb, c.m0 + q * 32, c.t, c.b);
+          if (lane == 0) {
+            if (p.tma_store == 2) tma_reduce_add5(&p.mapC[c.s], stg, c.n0 + cb, c.m0 + q * 32, c.t, c.b);
+            else tma_store5(&p.mapC[c.s], stg, c.n0 + cb, c.m0 + q * 32, c.t, c.b);
+          }
         }
         continue;
       }
@@ -625,6 +640,12 @@ cudaError_t launch_tf32_gemm(const Tf32Gemm& g, cudaStream_t stream) {
       ok = (reinterpret_cast<uintptr_t>(g.C[s]) & 15) == 0 && make_map(&p.mapC[s], g.C[s], dc, 32, 32, true) == cudaSuccess;
     }
     p.tma_store = ok && vec4 ? 1 : 0;
+    // in place with beta = 1 (U = U + ..., the last stage): the TMA unit adds the boxes into C,
+    // so D is never loaded; same single round-to-nearest add as alpha acc + D
+    static const bool no_reduce = getenv("KX_TF32_NOREDUCE") != nullptr;   // A/B experiments only
+    bool inplace = p.tma_store && g.beta == 1.0f && !no_reduce && g.ldd == g.ldc && g.sD_t == g.sC_t && g.sD_b == g.sC_b;
+    for (int s = 0; s < g.ns && inplace; ++s) inplace = g.D[s] == g.C[s];
+    if (inplace) p.tma_store = 2;
   }
   const int mS = g.kind == TF32_COL ? TBM : TBN;   // static operand rows per tile
   if ((e = make_map(&p.mapS_hi, g.S.hi, g.S, TBK, mS, true)) != cudaSuccess) return e;
