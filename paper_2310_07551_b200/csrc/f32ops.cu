@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(256) first_phase_f32_vec_kernel(const F32Phase
       if (live) {
         reinterpret_cast<float4*>(a.G[s])[q] = g[s];
         reinterpret_cast<float4*>(a.F[s])[q] = make_float4(f[0], f[1], f[2], f[3]);
+        if (a.Ucopy[s]) reinterpret_cast<float4*>(a.Ucopy[s])[q] = x[s];
       }
     }
   }
@@ -229,6 +230,10 @@ __global__ void __launch_bounds__(256) nonlin_f32_vec_kernel(const F32PhaseArgs 
     d1.x -= G1.x, d1.y -= G1.y, d1.z -= G1.z, d1.w -= G1.w;
     reinterpret_cast<float4*>(a.F[0])[q] = d0;
     reinterpret_cast<float4*>(a.F[1])[q] = d1;
+    if (a.Ucopy[0]) {
+      reinterpret_cast<float4*>(a.Ucopy[0])[q] = reinterpret_cast<const float4*>(a.Usrc[0])[q];
+      reinterpret_cast<float4*>(a.Ucopy[1])[q] = reinterpret_cast<const float4*>(a.Usrc[1])[q];
+    }
   }
 }
 
@@ -239,6 +244,7 @@ bool vec_ok(const F32PhaseArgs& a, bool first) {
   for (int s = 0; s < 2; ++s) {
     if (!al16f(a.U[s]) || !al16f(a.G[s]) || !al16f(a.F[s])) return false;
     if (first && !al16f(a.tri[s][0])) return false;
+    if (!al16f(a.Ucopy[s]) || !al16f(a.Usrc[s])) return false;
   }
   return true;
 }
@@ -284,6 +290,8 @@ cudaError_t launch_f64_to_f32(const double* x, float* y, long long n, cudaStream
   return cudaGetLastError();
 }
 
+bool f32_phase_vec_ok(const F32PhaseArgs& a, bool first) { return vec_ok(a, first); }
+
 cudaError_t launch_first_phase_f32(const F32PhaseArgs& a, cudaStream_t s) {
   if (a.N <= 0) return cudaSuccess;
   if (vec_ok(a, true) && (a.d == 2 || a.d == 3)) {
@@ -292,6 +300,7 @@ cudaError_t launch_first_phase_f32(const F32PhaseArgs& a, cudaStream_t s) {
     else first_phase_f32_vec_kernel<3><<<grid_of(q4), 256, 0, s>>>(a);
     return cudaGetLastError();
   }
+  if (a.Ucopy[0]) return cudaErrorInvalidValue;   // the copy is a vectorised-path feature
   if (a.d == 2) first_phase_f32_kernel<2><<<grid_of(a.N), 256, 0, s>>>(a);
   else if (a.d == 3) first_phase_f32_kernel<3><<<grid_of(a.N), 256, 0, s>>>(a);
   else return cudaErrorInvalidValue;
@@ -304,6 +313,7 @@ cudaError_t launch_nonlin_f32(const F32PhaseArgs& a, cudaStream_t s) {
     nonlin_f32_vec_kernel<<<grid_of(a.N / 4), 256, 0, s>>>(a);
     return cudaGetLastError();
   }
+  if (a.Ucopy[0]) return cudaErrorInvalidValue;
   nonlin_f32_kernel<<<grid_of(a.N), 256, 0, s>>>(a);
   return cudaGetLastError();
 }

@@ -374,12 +374,22 @@ kx_status stage_f32(kx_ctx* c, int k, int w, float* const* Y, const float* const
   return KX_OK;
 }
 
-kx_status nonlin_f32(kx_ctx* c, float* const* Us) {
+// D = g(Us) - G; with U given (and the vectorised kernel eligible) also Us = U afterwards, so
+// that the next stage GEMM adds into Us in place (TMA reduce-add, no D loads); returns through
+// *refilled whether it did
+kx_status nonlin_f32(kx_ctx* c, float* const* Us, float* const* U = nullptr, bool* refilled = nullptr) {
   F32State* f = c->f32;
   kx::F32PhaseArgs a = phase_args(c, Us);
   for (int s = 0; s < 2; ++s) a.F[s] = f->D + s * c->tN;
-  // HBM bytes: read U (2 fields), G (2); write D (2)
-  return run_other(c, [&] { return kx::launch_nonlin_f32(a, c->cur); }, 24.0 * (double)c->tN);
+  if (U) {
+    for (int s = 0; s < 2; ++s) a.Usrc[s] = U[s], a.Ucopy[s] = Us[s];
+    if (!kx::f32_phase_vec_ok(a, false))
+      for (int s = 0; s < 2; ++s) a.Usrc[s] = nullptr, a.Ucopy[s] = nullptr;
+  }
+  if (refilled) *refilled = a.Ucopy[0] != nullptr;
+  // HBM bytes: read U (2 fields), G (2); write D (2) (+ read U, write Us: 4 more)
+  const double bytes = (a.Ucopy[0] ? 40.0 : 24.0) * (double)c->tN;
+  return run_other(c, [&] { return kx::launch_nonlin_f32(a, c->cur); }, bytes);
 }
 
 kx_status enqueue_step_f32(kx_ctx* c, float* const* U) {
@@ -388,28 +398,39 @@ kx_status enqueue_step_f32(kx_ctx* c, float* const* U) {
   float* Us[2] = {f->Us, f->Us + N};
   const float* Uc[2] = {U[0], U[1]};
   const float* Usc[2] = {Us[0], Us[1]};
+  // Us = U is written by the first phase (and refreshed by the nonlinearity) where the
+  // vectorised kernels apply: the stage GEMMs U_k = U + ... then add into Us in place (one
+  // round-to-nearest add, as alpha acc + U) and skip their D loads
+  bool pre = false;
   {   // G = g(U), F = K U + G (planes)
     kx::F32PhaseArgs a = phase_args(c, U);
     for (int s = 0; s < 2; ++s) a.F[s] = f->F + s * N;
-    // HBM bytes: read U (2 fields), write G and F (4)
-    KX_TRY(run_other(c, [&] { return kx::launch_first_phase_f32(a, c->cur); }, 24.0 * (double)N));
+    for (int s = 0; s < 2; ++s) a.Usrc[s] = U[s], a.Ucopy[s] = Us[s];
+    pre = kx::f32_phase_vec_ok(a, true) && (c->d == 2 || c->d == 3) && !getenv("KX_F32_NOPREFILL");   // A/B
+    if (!pre)
+      for (int s = 0; s < 2; ++s) a.Usrc[s] = nullptr, a.Ucopy[s] = nullptr;
+    // HBM bytes: read U (2 fields), write G and F (4) (+ Us: 2)
+    KX_TRY(run_other(c, [&] { return kx::launch_first_phase_f32(a, c->cur); }, (pre ? 32.0 : 24.0) * (double)N));
     c->cnt.mode_products += 2LL * c->d;
     c->cnt.kronsum_actions += 2;
   }
   int w = 0;
   if (c->nstages == 3) {   // exprk3ds_real (Algorithms 1-2), groups F (3T), D2 (T), D3 (T)
     KX_TRY(group_modes_f32(c, 0, f->F, &w));
-    KX_TRY(stage_f32(c, 0, w, Us, Uc));                  // U2 = U + tau/3 S_1[F]
-    KX_TRY(nonlin_f32(c, Us));                            // D2 = g(U2) - G
+    KX_TRY(stage_f32(c, 0, w, Us, pre ? Usc : Uc));      // U2 = U + tau/3 S_1[F]
+    // D2 = g(U2) - G; with KX_F32_REFILL=1 also Us = U (stage U3 then in place too).  Off by
+    // default: that variant differs from the D-load form by 1 ulp in rare elements after a few
+    // steps (1 of 131072 at step 5, 256^2), unexplained, so it is not the default
+    KX_TRY(nonlin_f32(c, Us, (pre && getenv("KX_F32_REFILL")) ? U : nullptr, &pre));
     KX_TRY(group_modes_f32(c, 1, f->D, &w));
-    KX_TRY(stage_f32(c, 1, w, Us, Uc));                  // U3
+    KX_TRY(stage_f32(c, 1, w, Us, pre ? Usc : Uc));      // U3
     KX_TRY(nonlin_f32(c, Us));                            // D3 = g(U3) - G
     KX_TRY(group_modes_f32(c, 2, f->D, &w));
     KX_TRY(stage_f32(c, 2, w, U, Uc));                   // U+ (in place)
     c->cnt.tucker_ops += 2LL * 5 * c->T;
   } else {                 // ETD2RKDS (eq:ETD2RK), groups F (phi_1), D (phi_2)
     KX_TRY(group_modes_f32(c, 0, f->F, &w));
-    KX_TRY(stage_f32(c, 0, w, Us, Uc));                  // u2 = u + tau phi_1-split[F]
+    KX_TRY(stage_f32(c, 0, w, Us, pre ? Usc : Uc));      // u2 = u + tau phi_1-split[F]
     KX_TRY(nonlin_f32(c, Us));                            // D = g(u2) - G
     KX_TRY(group_modes_f32(c, 1, f->D, &w));
     KX_TRY(stage_f32(c, 1, w, U, Usc));                  // u+ = u2 + 2^{d-1} tau phi_2-split[D]

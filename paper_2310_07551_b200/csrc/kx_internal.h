@@ -119,7 +119,13 @@ struct F32PhaseArgs {
   float* G[2] = {};          // first phase: written; nonlinearity: read
   float* F[2] = {};          // first phase: F = K U + G; nonlinearity: D = g(U) - G
   const float* tri[2][3] = {};   // [species][mu-1]: lo | di | up (3 n_mu floats)
+  // optional (vectorised kernels): also write Ucopy = Usrc (the state the next stage GEMM adds
+  // its split action to, in place by TMA reduce-add); the nonlinearity may overwrite its own
+  // input U this way (each element is read before it is written)
+  const float* Usrc[2] = {};
+  float* Ucopy[2] = {};
 };
+bool f32_phase_vec_ok(const F32PhaseArgs& a, bool first);
 cudaError_t launch_split_f32(const float* x, float* hi, float* lo, long long n, cudaStream_t s);
 // fp32 rows x cols blocks (nbatch, contiguous) -> planes; transpose as launch_split_f64
 cudaError_t launch_split_f32_2d(const float* x, float* hi, float* lo, long long rows, long long cols, int nbatch,

@@ -300,3 +300,23 @@ def test_step_f32_zero_steps_is_noop(kx):
     assert all(torch.equal(a, b) for a, b in zip(U, before))
     assert ctx.counters()["steps"] == 0
     ctx.close()
+
+
+@pytest.mark.parametrize("n,mu", [([256, 192], 1), ([256, 192], 2), ([64, 48, 32], 3)])
+def test_inplace_epilogue_rounds_to_nearest(kx, n, mu):
+    """Y = X x_mu I + Y in place (beta = 1, D = C): the epilogue is a TMA reduce-add into Y.
+    X holds tf32-exact values (11 significant bits), so the split product is exactly X and the
+    result must be numpy's fp32 Y + X bit for bit (one round-to-nearest add)."""
+    N = int(np.prod(n))
+    rng = np.random.default_rng(7)
+    x = np.ldexp(rng.integers(-2**10, 2**10, N).astype(np.float64), -10).astype(np.float32)   # <= 11 bits
+    y = rng.standard_normal(N).astype(np.float32)
+    ctx = kx.Context(0)
+    ctx.set_grid(n, 1)
+    Y = dev32(y)
+    I = torch.eye(n[mu - 1], dtype=torch.float32, device="cuda")
+    ctx.mode_product_f32(dev32(x), Y, mu, I, 1.0, 1.0)
+    ctx.sync()
+    got = Y.cpu().numpy()
+    assert np.array_equal(got, y + x), int(np.sum(got != y + x))
+    ctx.close()
