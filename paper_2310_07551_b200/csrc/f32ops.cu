@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) first_phase_f32_kernel(const F32PhaseArgs
 // shuffles (lane 0 / 31 read theirs), the i_2 / i_3 neighbour lines as float4 loads that hit L2.
 // Arithmetic as first_phase_f32_kernel, point by point.
 template <int D>
-__global__ void __launch_bounds__(256) first_phase_f32_vec_kernel(const F32PhaseArgs a) {
+__global__ void __launch_bounds__(256, D == 3 ? 3 : 4) first_phase_f32_vec_kernel(const F32PhaseArgs a) {
   const int n1 = (int)a.n[0], n2 = (int)a.n[1], n3 = D == 3 ? (int)a.n[2] : 1;
   const int q4 = (int)(a.N / 4), l4 = n1 / 4, p4 = l4 * n2;   // quads: field, line, plane
   const int lane = threadIdx.x & 31;
