@@ -320,3 +320,25 @@ def test_inplace_epilogue_rounds_to_nearest(kx, n, mu):
     got = Y.cpu().numpy()
     assert np.array_equal(got, y + x), int(np.sum(got != y + x))
     ctx.close()
+
+
+def test_step_f32_rejects_misaligned_state(kx):
+    """U tensors off a 16-B boundary are refused (KX_ERR_INVALID) before anything is enqueued:
+    the vectorised pointwise kernels and the TMA loads / stores of the fp32 step need them."""
+    prob = inputs.make_problem("schnakenberg", 2, [96, 64], seed=4)
+    ctx = kx.Context(0)
+    ctx.set_grid(prob.n, 2)
+    for c in range(2):
+        for mu in range(prob.d):
+            ctx.set_direction_matrix(c, mu + 1, prob.A[c][mu])
+    ctx.set_model(prob.model, prob.params)
+    ctx.set_tau(2.0 / 6000, "etd3rkds")
+    N = int(np.prod(prob.n))
+    bufs = [torch.full((N + 1,), 7.0, dtype=torch.float32, device="cuda") for _ in range(2)]
+    U = [b[1:] for b in bufs]   # 4-byte offset
+    with pytest.raises(kx.KxError) as e:
+        ctx.step_f32(U, 1)
+    assert e.value.status == kx.KX_ERR_INVALID
+    ctx.sync()
+    assert all(bool(torch.all(b == 7.0)) for b in bufs)   # nothing written
+    ctx.close()
