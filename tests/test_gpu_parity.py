@@ -904,3 +904,23 @@ def test_fused_small_integrate_host_watchdog_profile(kx):
     c.set_profiling(False)
     assert prof["gemm_launches"] >= 1 and prof["gemm_flops"] > 0
     c.close()
+
+
+def test_integrate_host_tail_graph_follows_bank_and_buffers(ctx):
+    """The cached host-copy tail graph is rebuilt when the phi bank changes (kx_set_tau) and
+    when other host buffers are passed: results equal the device path at the new tau, and the
+    first host buffers are not written by the second call."""
+    prob = inputs.make_problem("schnakenberg", 2, [160, 96], seed=8)
+    setup_problem(ctx, prob, "etd3rkds", 1e-4)
+    a = [torch.from_numpy(u.copy()).pin_memory() for u in prob.U0]
+    ctx.integrate_host([p.numpy() for p in a], 2)
+    ctx.set_tau(3e-4, "etd3rkds")
+    Ud = [dev(u) for u in prob.U0]
+    for _ in range(2):
+        ctx.step(Ud)
+    b = [torch.from_numpy(u.copy()).pin_memory() for u in prob.U0]
+    snap = [p.clone() for p in a]
+    ctx.integrate_host([p.numpy() for p in b], 2)
+    for c in range(2):
+        assert relerr(b[c].numpy(), Ud[c].cpu().numpy()) <= 1e-14
+        assert torch.equal(a[c], snap[c])
